@@ -1,0 +1,172 @@
+/* knnjoin.h -- C ABI of libknnjoin.so, the B200 (sm_100a) hot path of the sparse KNN join of
+ * Wang et al., "Efficient K-Nearest Neighbor Join Algorithms for High Dimensional Sparse Data"
+ * (arxiv 1011.2807; /root/reference/PAPER.md).  SURVEY.md §8(b) is the contract.
+ *
+ * Operation (§3): for every sparse r in R return the k vectors s of S with the largest
+ * dot(r, s) = sum_i r[i]*s[i] (Eq. 1), ties broken toward the LOWER S id, zero scores never
+ * returned, rows with fewer than k positive scores padded with (id -1, score 0).  Scores are accumulated
+ * through the inverted lists I_d of S (Alg. 3), built here as an S-tiled,
+ * feature-major CSC ("tiled inverted index").
+ *
+ * Conventions for every entry point
+ *  - Every data pointer is a CUDA DEVICE pointer unless stated otherwise; every call is stream-ordered on
+ *    `stream` (a cudaStream_t passed as void*; NULL = legacy default stream) and returns without
+ *    synchronising, except knnjoin_validate_csr, which synchronises.
+ *  - The library allocates no device memory: the caller owns inputs, outputs, index storage and
+ *    workspaces, sized by the *_bytes queries (host-only computations, no device access).
+ *  - No exception or abort crosses the ABI.  Failures return a knnjoin_status; knnjoin_last_error()
+ *    returns a thread-local message for the last failing call on the calling thread.
+ *  - Sparse vectors are CSR rows of (feature d, weight w) pairs, features 0-based (PAPER.md:51 uses
+ *    1..D; reading c5) and strictly ascending, weights w > 0.  Structural validity
+ *    is checked only by knnjoin_validate_csr, never on the hot path; on the hot path R features >= d are
+ *    ignored (S has no such nonzero, so they add 0 to Eq. 1) and nothing is read out of bounds.
+ */
+#ifndef KNNJOIN_H
+#define KNNJOIN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  KNNJOIN_OK = 0,
+  KNNJOIN_ERR_ARG = 1,          /* null pointer, k out of range, bad option, negative size */
+  KNNJOIN_ERR_DIM = 2,          /* dimensionality mismatch / d <= 0 */
+  KNNJOIN_ERR_CSR = 3,          /* knnjoin_validate_csr found a structurally invalid row */
+  KNNJOIN_ERR_UNSUPPORTED = 4,  /* dtype combination or size outside the supported range */
+  KNNJOIN_ERR_WORKSPACE = 5,    /* storage / workspace smaller than the matching *_bytes query */
+  KNNJOIN_ERR_CUDA = 6          /* a CUDA runtime call failed; message carries cudaGetErrorString */
+} knnjoin_status;
+
+typedef enum {
+  KNNJOIN_BINARY = 0,  /* no values array: every stored feature has weight 1 */
+  KNNJOIN_INT8 = 1,    /* int8_t values, 1..127 */
+  KNNJOIN_FP32 = 2     /* float values, finite and > 0 */
+} knnjoin_dtype;
+
+/* A CSR matrix.  indptr: int64[n_rows+1], indptr[0] == 0, indptr[n_rows] == nnz, non-decreasing.
+ * indices: int32[nnz], strictly ascending within each row.  values: NULL for BINARY, int8_t[nnz] or
+ * float[nnz] otherwise.  All three are device pointers. */
+typedef struct {
+  int64_t n_rows;
+  int64_t nnz;
+  const int64_t* indptr;
+  const int32_t* indices;
+  const void* values;
+  knnjoin_dtype dtype;
+} knnjoin_csr;
+
+/* Build options.  tile: S ids per tile (the S-block of Alg. 1 mapped to a shared-memory score array);
+ * 0 = default 8192; must be a multiple of 2048 and <= 32768 (local ids are 15-bit).
+ * prune / alpha: reserved for the threshold-pruned mode; must be 0 / 0. */
+typedef struct {
+  int32_t tile;
+  int32_t prune;
+  float alpha;
+} knnjoin_options;
+
+/* Query options (all optional; pass NULL for defaults).
+ *  batch_rows: R rows per CTA batch (0 = auto: the largest of {8,6,4,2,1} whose score arrays fit in
+ *              shared memory for this tile width and k).
+ *  counters:   NULL, or a device int64_t[4] that the query ADDS into: [0] postings visited (Eq. 4 second
+ *              term), [1] candidate inserts into the top-k lists, [2] postings skipped by
+ *              pruning (0 in unpruned mode), [3] completions (0 in unpruned mode).
+ *  ev_begin / ev_end: NULL, or cudaEvent_t (as void*) recorded on `stream` immediately before and after
+ *              the score-accumulation + top-k kernel, so callers can time that kernel alone. */
+typedef struct {
+  int32_t batch_rows;
+  int64_t* counters;
+  void* ev_begin;
+  void* ev_end;
+} knnjoin_query_options;
+
+typedef struct knnjoin_index knnjoin_index; /* opaque HOST handle; borrows the caller's index storage */
+
+typedef struct {
+  int64_t n_s;          /* rows of S indexed */
+  int64_t s_id_base;    /* global id of S row 0 (S-sharded multi-GPU: the shard's first id) */
+  int32_t d;            /* dimensionality */
+  int32_t tile;         /* S ids per tile */
+  int64_t n_tiles;      /* ceil(n_s / tile) */
+  int64_t offsets;      /* entries of the offset table: d*(n_tiles+1)+1 */
+  int64_t unit_capacity;/* 16-byte posting units reserved in the storage (upper bound) */
+  int64_t storage_bytes;/* bytes of index storage the handle uses */
+  knnjoin_dtype s_dtype;
+} knnjoin_index_info;
+
+/* ---- index build: Create_Inverted_List_IIB (Alg. 3 lines 5-8) on the device ------ */
+
+/* Bytes of device storage the index of S needs (an upper bound computed on the host from n_rows, nnz, d
+ * and the tile width).  Returns 0 and sets knnjoin_last_error on invalid arguments. */
+size_t knnjoin_index_bytes(const knnjoin_csr* S, int32_t d, const knnjoin_options* opt);
+
+/* Bytes of device scratch knnjoin_build_index needs (sort buffers and scan temporaries). */
+size_t knnjoin_build_workspace_bytes(const knnjoin_csr* S, int32_t d, const knnjoin_options* opt);
+
+/* Build the tiled inverted index of S into `index_storage` (>= knnjoin_index_bytes bytes, 256-byte
+ * aligned) using `workspace` (>= knnjoin_build_workspace_bytes bytes).  Layout:
+ * for tile t (S ids [t*tile, (t+1)*tile)) and feature f, the postings of I_f restricted to the tile are a
+ * contiguous, 16-byte aligned slice of 15-bit local ids (+ uint8 values for INT8 S), padded with the
+ * sentinel 0xFFFF, permuted inside each 256-posting block so a warp's 32 lanes touch consecutive ids.
+ * s_id_base: global id of S row 0 (ids returned by queries are s_id_base + local row).
+ * S may be freed after the call's work completes on `stream`; the storage must outlive every query.
+ * S dtype must be BINARY or INT8 (FP32 S -> KNNJOIN_ERR_UNSUPPORTED).  *out receives a host handle
+ * to release with knnjoin_free_index. */
+knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64_t s_id_base, const knnjoin_options* opt,
+                                   void* index_storage, size_t storage_bytes, void* workspace, size_t workspace_bytes,
+                                   void* stream, knnjoin_index** out);
+
+knnjoin_status knnjoin_index_stats(const knnjoin_index* idx, knnjoin_index_info* out); /* host only */
+void knnjoin_free_index(knnjoin_index* idx); /* frees the HOST handle only; storage stays the caller's */
+
+/* ---- query: Find_Matches_IIB (Alg. 3 lines 9-17) for every r, fused with top-k ---- */
+
+/* Bytes of device scratch knnjoin_query needs for R and k. */
+size_t knnjoin_query_workspace_bytes(const knnjoin_index* idx, const knnjoin_csr* R, int32_t k,
+                                     const knnjoin_query_options* qopt);
+
+/* For every row r of R (1 <= k <= 256) write, in rank order (score desc, id asc):
+ *   out_ids[r*k + i]    int32  global S id, or -1 for padding;
+ *   out_scores[r*k + i] float  dot(r, s) (exact for BINARY/INT8 R; for FP32 R the per-row fixed-point
+ *                              sum / scale, relative error ~1e-8);
+ *   out_keys[r*k + i]   uint64 (optional, may be NULL) the packed ordering key
+ *                              (score_u32 << 32) | (0xFFFFFFFF - global_id), 0 for padding, as consumed by
+ *                              knnjoin_merge (S-sharded multi-GPU).
+ * out_ids / out_scores may be NULL when out_keys is given.  R dtype: BINARY, INT8 or FP32.
+ * Integer (BINARY/INT8 x BINARY/INT8) scores must fit in 32 bits: d * 127 * 127 < 2^32, else UNSUPPORTED.
+ * Empty R: nothing is written.  Empty S: every row is padding. */
+knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr* R, int32_t k,
+                             const knnjoin_query_options* qopt, uint64_t* out_keys, int32_t* out_ids,
+                             float* out_scores, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- S-sharded merge: P partial top-k lists per row -> global top-k ---------------- */
+
+size_t knnjoin_merge_workspace_bytes(const knnjoin_csr* R);
+
+/* keys: uint64[P][n_rows][k] (each [n_rows][k] slab is one shard's out_keys, e.g. gathered by an NCCL
+ * all-gather).  Writes the global top-k per row into out_keys / out_ids / out_scores (any may be NULL
+ * but not all), using R, d (the index dimensionality) and s_dtype (the dtype of S) only to recover the
+ * per-row score scale, exactly as knnjoin_query computed it.
+ * The merge is exact: keys encode (score, lower-id-wins) as one unsigned integer. */
+knnjoin_status knnjoin_merge(const uint64_t* keys, int32_t P, const knnjoin_csr* R, int32_t d,
+                             knnjoin_dtype s_dtype, int32_t k, uint64_t* out_keys, int32_t* out_ids, float* out_scores, void* workspace,
+                             size_t workspace_bytes, void* stream);
+
+/* ---- validation (not on the hot path) ------------------------------------------------------------- */
+
+/* Checks, on the device, that `m` is a valid CSR for dimensionality d: indptr[0]==0, non-decreasing,
+ * indptr[n_rows]==nnz; indices strictly ascending within each row and in [0, d); values > 0 (and finite
+ * for FP32).  SYNCHRONISES `stream`.  Returns KNNJOIN_OK, or KNNJOIN_ERR_CSR with *bad_row (host
+ * pointer, may be NULL) set to the first offending row (-1 for a global indptr problem). */
+knnjoin_status knnjoin_validate_csr(const knnjoin_csr* m, int32_t d, void* stream, int64_t* bad_row);
+
+const char* knnjoin_last_error(void);
+const char* knnjoin_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KNNJOIN_H */

@@ -1,0 +1,259 @@
+"""ctypes binding of libknnjoin.so (include/knnjoin.h).  Marshalling only: every step of the path runs in the
+library's CUDA kernels; this module allocates the caller-owned buffers with torch and passes raw pointers,
+sizes and the current CUDA stream."""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libknnjoin.so")
+
+BINARY, INT8, FP32 = 0, 1, 2
+_DTYPE_NAMES = {"binary": BINARY, "int8": INT8, "fp32": FP32}
+
+STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_DIM", 3: "ERR_CSR", 4: "ERR_UNSUPPORTED", 5: "ERR_WORKSPACE", 6: "ERR_CUDA"}
+
+
+class KnnJoinError(RuntimeError):
+    def __init__(self, status: int, where: str, message: str):
+        super().__init__(f"{where}: {STATUS.get(status, status)}: {message}")
+        self.status = status
+
+
+class _CSR(ctypes.Structure):
+    _fields_ = [("n_rows", ctypes.c_int64), ("nnz", ctypes.c_int64), ("indptr", ctypes.c_void_p),
+                ("indices", ctypes.c_void_p), ("values", ctypes.c_void_p), ("dtype", ctypes.c_int)]
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("tile", ctypes.c_int32), ("prune", ctypes.c_int32), ("alpha", ctypes.c_float)]
+
+
+class _QueryOptions(ctypes.Structure):
+    _fields_ = [("batch_rows", ctypes.c_int32), ("counters", ctypes.c_void_p), ("ev_begin", ctypes.c_void_p),
+                ("ev_end", ctypes.c_void_p)]
+
+
+class _IndexInfo(ctypes.Structure):
+    _fields_ = [("n_s", ctypes.c_int64), ("s_id_base", ctypes.c_int64), ("d", ctypes.c_int32),
+                ("tile", ctypes.c_int32), ("n_tiles", ctypes.c_int64), ("offsets", ctypes.c_int64),
+                ("unit_capacity", ctypes.c_int64), ("storage_bytes", ctypes.c_int64), ("s_dtype", ctypes.c_int)]
+
+
+def library_path() -> str:
+    return _SO
+
+
+def _load():
+    if not os.path.exists(_SO):
+        raise ImportError(f"{_SO} is missing: the CUDA library must be built (python __graft_entry__.py build); "
+                          "there is no CPU fallback")
+    L = ctypes.CDLL(_SO)
+    P = ctypes.POINTER
+    c = ctypes
+    L.knnjoin_index_bytes.argtypes = [P(_CSR), c.c_int32, P(_Options)]
+    L.knnjoin_index_bytes.restype = c.c_size_t
+    L.knnjoin_build_workspace_bytes.argtypes = [P(_CSR), c.c_int32, P(_Options)]
+    L.knnjoin_build_workspace_bytes.restype = c.c_size_t
+    L.knnjoin_build_index.argtypes = [P(_CSR), c.c_int32, c.c_int64, P(_Options), c.c_void_p, c.c_size_t, c.c_void_p,
+                                      c.c_size_t, c.c_void_p, P(c.c_void_p)]
+    L.knnjoin_build_index.restype = c.c_int
+    L.knnjoin_index_stats.argtypes = [c.c_void_p, P(_IndexInfo)]
+    L.knnjoin_index_stats.restype = c.c_int
+    L.knnjoin_free_index.argtypes = [c.c_void_p]
+    L.knnjoin_free_index.restype = None
+    L.knnjoin_query_workspace_bytes.argtypes = [c.c_void_p, P(_CSR), c.c_int32, P(_QueryOptions)]
+    L.knnjoin_query_workspace_bytes.restype = c.c_size_t
+    L.knnjoin_query.argtypes = [c.c_void_p, P(_CSR), c.c_int32, P(_QueryOptions), c.c_void_p, c.c_void_p, c.c_void_p,
+                                c.c_void_p, c.c_size_t, c.c_void_p]
+    L.knnjoin_query.restype = c.c_int
+    L.knnjoin_merge_workspace_bytes.argtypes = [P(_CSR)]
+    L.knnjoin_merge_workspace_bytes.restype = c.c_size_t
+    L.knnjoin_merge.argtypes = [c.c_void_p, c.c_int32, P(_CSR), c.c_int32, c.c_int, c.c_int32, c.c_void_p, c.c_void_p,
+                                c.c_void_p, c.c_void_p, c.c_size_t, c.c_void_p]
+    L.knnjoin_merge.restype = c.c_int
+    L.knnjoin_validate_csr.argtypes = [P(_CSR), c.c_int32, c.c_void_p, P(c.c_int64)]
+    L.knnjoin_validate_csr.restype = c.c_int
+    L.knnjoin_last_error.argtypes = []
+    L.knnjoin_last_error.restype = c.c_char_p
+    L.knnjoin_version.argtypes = []
+    L.knnjoin_version.restype = c.c_char_p
+    return L
+
+
+_lib = _load()
+
+EXPORTS = ["knnjoin_index_bytes", "knnjoin_build_workspace_bytes", "knnjoin_build_index", "knnjoin_index_stats",
+           "knnjoin_free_index", "knnjoin_query_workspace_bytes", "knnjoin_query", "knnjoin_merge_workspace_bytes",
+           "knnjoin_merge", "knnjoin_validate_csr", "knnjoin_last_error", "knnjoin_version"]
+
+
+def knnjoin_last_error() -> str:
+    return _lib.knnjoin_last_error().decode()
+
+
+def knnjoin_version() -> str:
+    return _lib.knnjoin_version().decode()
+
+
+def _check(status: int, where: str):
+    if status != 0:
+        raise KnnJoinError(status, where, knnjoin_last_error())
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream)
+
+
+@dataclass
+class DeviceCSR:
+    """A CSR matrix whose arrays are device tensors (indptr int64, indices int32, values int8/float32/None)."""
+    indptr: torch.Tensor
+    indices: torch.Tensor
+    values: torch.Tensor | None
+    dtype: int
+
+    @property
+    def n_rows(self) -> int:
+        return self.indptr.numel() - 1
+
+    @property
+    def nnz(self) -> int:
+        return self.indices.numel()
+
+    @staticmethod
+    def from_arrays(indptr, indices, values=None, device="cuda", non_blocking=False) -> "DeviceCSR":
+        """Copy host arrays (numpy or torch) to ``device``.  values: None (binary), int8 or float32."""
+        def t(x, dt):
+            if isinstance(x, np.ndarray):
+                x = torch.from_numpy(np.ascontiguousarray(x))
+            return x.to(device=device, dtype=dt, non_blocking=non_blocking)
+        ip = t(indptr, torch.int64)
+        ix = t(indices, torch.int32)
+        if values is None:
+            return DeviceCSR(ip, ix, None, BINARY)
+        vdt = values.dtype
+        is_int8 = (vdt == np.int8) if isinstance(values, np.ndarray) else (vdt == torch.int8)
+        if is_int8:
+            return DeviceCSR(ip, ix, t(values, torch.int8), INT8)
+        return DeviceCSR(ip, ix, t(values, torch.float32), FP32)
+
+    @staticmethod
+    def from_host(h, device="cuda", non_blocking=False) -> "DeviceCSR":
+        return DeviceCSR.from_arrays(h.indptr, h.indices, h.values, device, non_blocking)
+
+    def _c(self) -> _CSR:
+        return _CSR(self.n_rows, self.nnz, self.indptr.data_ptr(), self.indices.data_ptr() if self.nnz else 0,
+                    self.values.data_ptr() if (self.values is not None and self.nnz) else 0, self.dtype)
+
+
+class Index:
+    """Host handle + caller-owned device storage of a built index (knnjoin_build_index)."""
+
+    def __init__(self, handle: int, storage: torch.Tensor, d: int, s_dtype: int, n_s: int, s_id_base: int):
+        self._h = ctypes.c_void_p(handle)
+        self.storage = storage
+        self.d = d
+        self.s_dtype = s_dtype
+        self.n_s = n_s
+        self.s_id_base = s_id_base
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.knnjoin_free_index(self._h)
+            self._h = None
+
+
+def _empty_u8(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+def knnjoin_build_index(S: DeviceCSR, d: int, s_id_base: int = 0, tile: int = 0, stream=None,
+                        workspace: torch.Tensor | None = None) -> Index:
+    cS = S._c()
+    opt = _Options(tile, 0, 0.0)
+    nbytes = _lib.knnjoin_index_bytes(ctypes.byref(cS), d, ctypes.byref(opt))
+    if nbytes == 0:
+        raise KnnJoinError(1, "knnjoin_index_bytes", knnjoin_last_error())
+    wbytes = _lib.knnjoin_build_workspace_bytes(ctypes.byref(cS), d, ctypes.byref(opt))
+    if wbytes == 0:
+        raise KnnJoinError(1, "knnjoin_build_workspace_bytes", knnjoin_last_error())
+    dev = S.indptr.device
+    storage = _empty_u8(nbytes, dev)
+    ws = workspace if (workspace is not None and workspace.numel() >= wbytes) else _empty_u8(wbytes, dev)
+    out = ctypes.c_void_p()
+    _check(_lib.knnjoin_build_index(ctypes.byref(cS), d, s_id_base, ctypes.byref(opt), storage.data_ptr(), nbytes,
+                                    ws.data_ptr(), ws.numel(), _stream_ptr(stream), ctypes.byref(out)),
+           "knnjoin_build_index")
+    # keep the workspace alive until the stream has consumed it
+    ws.record_stream(torch.cuda.current_stream() if stream is None else stream)
+    return Index(out.value, storage, d, S.dtype, S.n_rows, s_id_base)
+
+
+def knnjoin_index_stats(index: Index) -> dict:
+    info = _IndexInfo()
+    _check(_lib.knnjoin_index_stats(index.handle, ctypes.byref(info)), "knnjoin_index_stats")
+    return {f: getattr(info, f) for f, _ in _IndexInfo._fields_}
+
+
+def knnjoin_query(index: Index, R: DeviceCSR, k: int, want_keys: bool = False, want_ids: bool = True,
+                  batch_rows: int = 0, counters: torch.Tensor | None = None, events=None, stream=None,
+                  workspace: torch.Tensor | None = None):
+    """Returns (ids int32 [n,k], scores float32 [n,k], keys uint64-as-int64 [n,k] or None)."""
+    cR = R._c()
+    qo = _QueryOptions(batch_rows, counters.data_ptr() if counters is not None else 0,
+                       events[0].cuda_event if events else 0, events[1].cuda_event if events else 0)
+    wbytes = _lib.knnjoin_query_workspace_bytes(index.handle, ctypes.byref(cR), k, ctypes.byref(qo))
+    if wbytes == 0:
+        raise KnnJoinError(1, "knnjoin_query_workspace_bytes", knnjoin_last_error())
+    dev = R.indptr.device
+    n = R.n_rows
+    ids = torch.empty((n, k), dtype=torch.int32, device=dev) if want_ids else None
+    scores = torch.empty((n, k), dtype=torch.float32, device=dev) if want_ids else None
+    keys = torch.empty((n, k), dtype=torch.int64, device=dev) if want_keys else None
+    ws = workspace if (workspace is not None and workspace.numel() >= wbytes) else _empty_u8(wbytes, dev)
+    _check(_lib.knnjoin_query(index.handle, ctypes.byref(cR), k, ctypes.byref(qo),
+                              keys.data_ptr() if keys is not None else 0, ids.data_ptr() if ids is not None else 0,
+                              scores.data_ptr() if scores is not None else 0, ws.data_ptr(), ws.numel(),
+                              _stream_ptr(stream)), "knnjoin_query")
+    ws.record_stream(torch.cuda.current_stream() if stream is None else stream)
+    return ids, scores, keys
+
+
+def knnjoin_merge(keys: torch.Tensor, R: DeviceCSR, d: int, s_dtype: int, k: int, want_keys: bool = False,
+                  stream=None):
+    """keys: int64 view of uint64 [P, n, k].  Returns (ids, scores, merged keys or None)."""
+    P = keys.shape[0]
+    cR = R._c()
+    dev = keys.device
+    n = R.n_rows
+    wbytes = _lib.knnjoin_merge_workspace_bytes(ctypes.byref(cR))
+    ws = _empty_u8(wbytes, dev)
+    ids = torch.empty((n, k), dtype=torch.int32, device=dev)
+    scores = torch.empty((n, k), dtype=torch.float32, device=dev)
+    out_keys = torch.empty((n, k), dtype=torch.int64, device=dev) if want_keys else None
+    _check(_lib.knnjoin_merge(keys.data_ptr(), P, ctypes.byref(cR), d, s_dtype, k,
+                              out_keys.data_ptr() if out_keys is not None else 0, ids.data_ptr(), scores.data_ptr(),
+                              ws.data_ptr(), ws.numel(), _stream_ptr(stream)), "knnjoin_merge")
+    ws.record_stream(torch.cuda.current_stream() if stream is None else stream)
+    return ids, scores, out_keys
+
+
+def knnjoin_validate_csr(m: DeviceCSR, d: int, stream=None):
+    """Returns (status, bad_row): status 0 = valid, 3 = ERR_CSR with the first bad row."""
+    bad = ctypes.c_int64(-1)
+    st = _lib.knnjoin_validate_csr(ctypes.byref(m._c()), d, _stream_ptr(stream), ctypes.byref(bad))
+    if st not in (0, 3):
+        _check(st, "knnjoin_validate_csr")
+    return st, bad.value

@@ -1,0 +1,60 @@
+// common.cuh -- internal declarations shared by the translation units of libknnjoin.so.
+// Nothing here is shared with oracle/ (the CPU oracle); see DESIGN.md "Boundary".
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/knnjoin.h"
+
+#define KJ_API extern "C" __attribute__((visibility("default")))
+
+namespace kj {
+
+constexpr int kWarps = 16;             // warps per CTA of the accumulation kernel
+constexpr int kThreads = kWarps * 32;  // 512
+constexpr int kCap = kThreads;         // posting runs staged in shared memory per chunk (one per thread)
+constexpr int kMaxK = 256;
+constexpr int kDefaultTile = 8192;
+constexpr int kMaxTile = 32768;        // local ids are 15-bit; 0xFFFF is the padding sentinel
+constexpr int kTileQuantum = 2048;     // tile must split into kWarps column strips of 128-column chunks
+constexpr uint16_t kSentinel = 0xFFFF;
+constexpr uint64_t kKeyFloor = 0x00000000FFFFFFFFull;  // score 0 with every id: admits nothing
+constexpr double kFixedOne = 1073741824.0;              // 2^30: per-row fixed-point scale numerator
+
+void set_error(const char* fmt, ...);
+knnjoin_status cuda_fail(cudaError_t e, const char* what);
+
+__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// host-side layout of the index storage (all offsets 256-byte aligned)
+struct IndexLayout {
+  int64_t n_tiles = 0, n_off = 0, unit_cap = 0;
+  size_t off_at = 0, df_at = 0, ids_at = 0, vals_at = 0, total = 0;
+};
+bool index_layout(const knnjoin_csr* S, int32_t d, int32_t tile, IndexLayout* L);
+int32_t resolve_tile(const knnjoin_options* opt);
+
+// per-row score scale: sigma[r] = 2^30 / (sum_d r_d * smax) for FP32 R,
+// 1 for integer R.  inv_sigma[r] = 1 / sigma[r] converts a fixed-point sum back to a score.
+void launch_row_scale(const knnjoin_csr* R, int32_t d, int32_t smax, double* sigma, double* inv_sigma,
+                      cudaStream_t st);
+
+// finalize / merge helpers implemented in merge.cu
+int ks_for_k(int32_t k);
+
+}  // namespace kj
+
+struct knnjoin_index {
+  int64_t n_s = 0, s_id_base = 0;
+  int32_t d = 0, tile = 0;
+  int64_t n_tiles = 0, n_off = 0, unit_cap = 0;
+  knnjoin_dtype s_dtype = KNNJOIN_BINARY;
+  const uint32_t* off = nullptr;  // [n_off] posting-unit (16 B) offsets, feature-major: f*(n_tiles+1)+t
+  const int32_t* df = nullptr;    // [d] |I_d| (document frequency of each feature in S)
+  const uint16_t* ids = nullptr;  // [unit_cap*8] 15-bit local S ids, 0xFFFF padding
+  const uint8_t* vals = nullptr;  // [unit_cap*8] INT8 S weights (nullptr for BINARY S)
+  size_t storage_bytes = 0;
+};

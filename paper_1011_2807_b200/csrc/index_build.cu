@@ -1,0 +1,281 @@
+// index_build.cu -- K1: the tiled inverted index of S, built on the device.
+//
+// This is Create_Inverted_List_IIB (Alg. 3 lines 5-8: "for every feature (d, w) of
+// every s insert (s, w) into I_d") re-shaped for the GPU: the lists are partitioned into S-id tiles of
+// `tile` ids (the analogue of Alg. 1's S blocks, sized so one tile's score array fits in shared memory)
+// and laid out feature-major so that slice (f, t) = I_f ∩ tile t is contiguous:
+//
+//   off[f*(n_tiles+1) + t] .. off[f*(n_tiles+1) + t + 1]   16-byte posting units of slice (f, t)
+//   ids[8*u .. 8*u+8)                                        8 local ids (s - t*tile) per unit, 0xFFFF pad
+//   vals[8*u .. 8*u+8)                                       INT8 S weights (same positions)
+//
+// Steps (all stream-ordered, integer, deterministic):
+//   1. k_count     key(s, f) = f*(n_tiles+1) + t(s); histogram of keys; df[f] (= |I_f|)
+//   2. k_units     units(key) = ceil(count/8)   (16-byte alignment of every slice)
+//   3. CUB exclusive scans: off = scan(units), first = scan(count)
+//   4. CUB stable radix sort of (key, s) pairs -- CSR order is ascending s, so each key's postings come
+//      out in ascending s (Alg. 3 inserts "in B_s scan order")
+//   5. k_scatter   posting of sorted rank rho inside slice goes to block rho/256, and inside a block of m
+//      units to lane i = rho%m, slot j = rho/m (unit i holds sorted postings i, i+m, ..., i+7m): when a
+//      warp's lane i loads unit i and issues atomic j, the 32 lanes hit 32 consecutive ids of a dense
+//      slice -> 32 distinct shared-memory banks.
+// The paper counts this as Eq. 4's first term, sum |s_i| postings.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace kj {
+
+int32_t resolve_tile(const knnjoin_options* opt) {
+  int32_t t = (opt && opt->tile) ? opt->tile : kDefaultTile;
+  if (t <= 0 || t > kMaxTile || t % kTileQuantum != 0) return -1;
+  return t;
+}
+
+bool index_layout(const knnjoin_csr* S, int32_t d, int32_t tile, IndexLayout* L) {
+  if (!S || d <= 0 || tile <= 0 || S->n_rows < 0 || S->nnz < 0) return false;
+  L->n_tiles = (S->n_rows + tile - 1) / tile;
+  L->n_off = (int64_t)d * (L->n_tiles + 1) + 1;
+  int64_t slices = (int64_t)d * L->n_tiles;
+  int64_t nonempty = S->nnz < slices ? S->nnz : slices;
+  L->unit_cap = S->nnz / 8 + nonempty + 1;  // sum ceil(c/8) <= nnz/8 + 7/8 * #non-empty slices
+  size_t at = 0;
+  L->off_at = at;
+  at = align_up(at + sizeof(uint32_t) * (size_t)L->n_off, 256);
+  L->df_at = at;
+  at = align_up(at + sizeof(int32_t) * (size_t)d, 256);
+  L->ids_at = at;
+  at = align_up(at + 16 * (size_t)L->unit_cap, 256);
+  L->vals_at = at;
+  if (S->dtype == KNNJOIN_INT8) at = align_up(at + 8 * (size_t)L->unit_cap, 256);
+  L->total = at;
+  return true;
+}
+
+namespace {
+
+struct BuildWs {
+  size_t counts_at, units_at, first_at, ka_at, kb_at, va_at, vb_at, cub_at, cub_bytes, total;
+};
+
+int end_bit_for(int64_t max_key) {
+  int b = 1;
+  while (b < 32 && ((int64_t)1 << b) <= max_key) ++b;
+  return b;
+}
+
+bool build_ws_layout(const knnjoin_csr* S, const IndexLayout& L, BuildWs* W) {
+  size_t nnz = (size_t)S->nnz, n_off = (size_t)L.n_off;
+  size_t sort_bytes = 0, scan_bytes = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)nnz, 0,
+                                                  end_bit_for(L.n_off - 1));
+  if (e != cudaSuccess) return false;
+  e = cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n_off);
+  if (e != cudaSuccess) return false;
+  size_t at = 0;
+  W->counts_at = at; at = align_up(at + 4 * n_off, 256);
+  W->units_at = at;  at = align_up(at + 4 * n_off, 256);
+  W->first_at = at;  at = align_up(at + 4 * n_off, 256);
+  W->ka_at = at;     at = align_up(at + 4 * nnz, 256);
+  W->kb_at = at;     at = align_up(at + 4 * nnz, 256);
+  W->va_at = at;     at = align_up(at + 4 * nnz, 256);
+  W->vb_at = at;     at = align_up(at + 4 * nnz, 256);
+  W->cub_at = at;
+  W->cub_bytes = sort_bytes > scan_bytes ? sort_bytes : scan_bytes;
+  at = align_up(at + W->cub_bytes, 256);
+  W->total = at;
+  return true;
+}
+
+bool check_build_args(const knnjoin_csr* S, int32_t d, const knnjoin_options* opt, int32_t* tile) {
+  if (!S) { set_error("S is NULL"); return false; }
+  if (d <= 0) { set_error("d must be > 0 (got %d)", d); return false; }
+  if (d >= (1 << 24)) { set_error("d must be < 2^24 (feature ids share a word with an 8-row mask)"); return false; }
+  if (S->n_rows < 0 || S->nnz < 0) { set_error("negative S size"); return false; }
+  if (S->dtype != KNNJOIN_BINARY && S->dtype != KNNJOIN_INT8) {
+    set_error("S dtype %d unsupported: S must be BINARY or INT8 (DESIGN.md: fixed-point scores)", (int)S->dtype);
+    return false;
+  }
+  if (S->nnz >= ((int64_t)1 << 31)) { set_error("nnz(S) must be < 2^31 per index (shard S)"); return false; }
+  *tile = resolve_tile(opt);
+  if (*tile < 0) { set_error("tile must be a multiple of %d in [%d, %d]", kTileQuantum, kTileQuantum, kMaxTile); return false; }
+  if (opt && (opt->prune != 0)) { set_error("pruned mode is not available in this build (options.prune must be 0)"); return false; }
+  if ((int64_t)d * ((S->n_rows + *tile - 1) / *tile + 1) + 1 >= ((int64_t)1 << 31)) {
+    set_error("d * (n_tiles+1) too large for 32-bit slice keys; shard S or raise the tile width");
+    return false;
+  }
+  return true;
+}
+
+// warp per S row
+__global__ void k_count(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                        const int8_t* __restrict__ values, int64_t n_s, int32_t d, int32_t tile, int64_t n_tiles,
+                        uint32_t* __restrict__ counts, int32_t* __restrict__ df, uint32_t* __restrict__ keys,
+                        uint32_t* __restrict__ vals, uint32_t sentinel_key) {
+  int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (row >= n_s) return;
+  int64_t t = row / tile;
+  uint32_t local = (uint32_t)(row - t * tile);
+  for (int64_t j = indptr[row] + lane; j < indptr[row + 1]; j += 32) {
+    int32_t f = indices[j];
+    if (f >= 0 && f < d) {
+      uint32_t key = (uint32_t)((int64_t)f * (n_tiles + 1) + t);
+      atomicAdd(&counts[key], 1u);
+      atomicAdd(&df[f], 1);
+      uint32_t v = values ? (uint32_t)(uint8_t)values[j] : 0u;
+      keys[j] = key;
+      vals[j] = local | (v << 16);
+    } else {
+      keys[j] = sentinel_key;
+      vals[j] = 0;
+    }
+  }
+}
+
+__global__ void k_units(const uint32_t* __restrict__ counts, uint32_t* __restrict__ units, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) units[i] = (counts[i] + 7u) >> 3;
+}
+
+__global__ void k_scatter(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, int64_t nnz,
+                          const uint32_t* __restrict__ off, const uint32_t* __restrict__ first,
+                          uint32_t sentinel_key, uint16_t* __restrict__ ids, uint8_t* __restrict__ wvals) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nnz) return;
+  uint32_t key = keys[i];
+  if (key >= sentinel_key) return;
+  uint32_t rank = (uint32_t)i - first[key];
+  uint32_t u0 = off[key];
+  uint32_t U = off[key + 1] - u0;
+  uint32_t beta = rank >> 8, iota = rank & 255u;
+  uint32_t m = U - 32u * beta;
+  if (m > 32u) m = 32u;
+  uint32_t ii = iota % m, jj = iota / m;
+  size_t pos = (size_t)u0 * 8 + (size_t)beta * 256 + ii * 8 + jj;
+  uint32_t v = vals[i];
+  ids[pos] = (uint16_t)(v & 0xFFFFu);
+  if (wvals) wvals[pos] = (uint8_t)(v >> 16);
+}
+
+}  // namespace
+}  // namespace kj
+
+using namespace kj;
+
+KJ_API size_t knnjoin_index_bytes(const knnjoin_csr* S, int32_t d, const knnjoin_options* opt) {
+  int32_t tile;
+  if (!check_build_args(S, d, opt, &tile)) return 0;
+  IndexLayout L;
+  if (!index_layout(S, d, tile, &L)) { set_error("bad index layout arguments"); return 0; }
+  return L.total;
+}
+
+KJ_API size_t knnjoin_build_workspace_bytes(const knnjoin_csr* S, int32_t d, const knnjoin_options* opt) {
+  int32_t tile;
+  if (!check_build_args(S, d, opt, &tile)) return 0;
+  IndexLayout L;
+  BuildWs W;
+  if (!index_layout(S, d, tile, &L) || !build_ws_layout(S, L, &W)) { set_error("workspace sizing failed"); return 0; }
+  return W.total;
+}
+
+KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64_t s_id_base,
+                                          const knnjoin_options* opt, void* storage, size_t storage_bytes,
+                                          void* workspace, size_t workspace_bytes, void* stream,
+                                          knnjoin_index** out) {
+  if (!out) { set_error("out is NULL"); return KNNJOIN_ERR_ARG; }
+  *out = nullptr;
+  int32_t tile;
+  if (!check_build_args(S, d, opt, &tile)) return (S && d <= 0) ? KNNJOIN_ERR_DIM : KNNJOIN_ERR_ARG;
+  if (S->dtype != KNNJOIN_BINARY && S->dtype != KNNJOIN_INT8) return KNNJOIN_ERR_UNSUPPORTED;
+  if (s_id_base < 0 || s_id_base + S->n_rows > (int64_t)0x7FFFFFFF) {
+    set_error("global S ids must fit in int32 (s_id_base + n_rows < 2^31)");
+    return KNNJOIN_ERR_UNSUPPORTED;
+  }
+  if (S->n_rows > 0 && (!S->indptr || (S->nnz > 0 && !S->indices))) { set_error("S pointers are NULL"); return KNNJOIN_ERR_ARG; }
+  if (S->dtype == KNNJOIN_INT8 && S->nnz > 0 && !S->values) { set_error("INT8 S needs values"); return KNNJOIN_ERR_ARG; }
+  IndexLayout L;
+  BuildWs W;
+  if (!index_layout(S, d, tile, &L) || !build_ws_layout(S, L, &W)) { set_error("layout failed"); return KNNJOIN_ERR_ARG; }
+  if (!storage || storage_bytes < L.total) { set_error("index storage %zu < %zu bytes", storage_bytes, L.total); return KNNJOIN_ERR_WORKSPACE; }
+  if (!workspace || workspace_bytes < W.total) { set_error("build workspace %zu < %zu bytes", workspace_bytes, W.total); return KNNJOIN_ERR_WORKSPACE; }
+  if (((uintptr_t)storage & 255) || ((uintptr_t)workspace & 255)) { set_error("storage and workspace must be 256-byte aligned"); return KNNJOIN_ERR_ARG; }
+
+  cudaStream_t st = (cudaStream_t)stream;
+  char* sb = (char*)storage;
+  char* wb = (char*)workspace;
+  uint32_t* off = (uint32_t*)(sb + L.off_at);
+  int32_t* df = (int32_t*)(sb + L.df_at);
+  uint16_t* ids = (uint16_t*)(sb + L.ids_at);
+  uint8_t* vals = S->dtype == KNNJOIN_INT8 ? (uint8_t*)(sb + L.vals_at) : nullptr;
+  uint32_t* counts = (uint32_t*)(wb + W.counts_at);
+  uint32_t* units = (uint32_t*)(wb + W.units_at);
+  uint32_t* first = (uint32_t*)(wb + W.first_at);
+  uint32_t* ka = (uint32_t*)(wb + W.ka_at);
+  uint32_t* kb = (uint32_t*)(wb + W.kb_at);
+  uint32_t* va = (uint32_t*)(wb + W.va_at);
+  uint32_t* vb = (uint32_t*)(wb + W.vb_at);
+  void* cubtmp = wb + W.cub_at;
+  uint32_t sentinel_key = (uint32_t)(L.n_off - 1);
+
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(counts, 0, 4 * (size_t)L.n_off, st)) != cudaSuccess) return cuda_fail(e, "memset counts");
+  if ((e = cudaMemsetAsync(df, 0, 4 * (size_t)d, st)) != cudaSuccess) return cuda_fail(e, "memset df");
+  if ((e = cudaMemsetAsync(ids, 0xFF, 16 * (size_t)L.unit_cap, st)) != cudaSuccess) return cuda_fail(e, "memset ids");
+  if (vals && (e = cudaMemsetAsync(vals, 0, 8 * (size_t)L.unit_cap, st)) != cudaSuccess) return cuda_fail(e, "memset vals");
+  if (S->n_rows > 0) {
+    int64_t threads = S->n_rows * 32;
+    k_count<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(S->indptr, S->indices, (const int8_t*)S->values,
+                                                             S->n_rows, d, tile, L.n_tiles, counts, df, ka, va,
+                                                             sentinel_key);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_count");
+  }
+  k_units<<<(unsigned)((L.n_off + 255) / 256), 256, 0, st>>>(counts, units, L.n_off);
+  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_units");
+  size_t tb = W.cub_bytes;
+  if ((e = cub::DeviceScan::ExclusiveSum(cubtmp, tb, units, off, (int)L.n_off, st)) != cudaSuccess) return cuda_fail(e, "scan off");
+  tb = W.cub_bytes;
+  if ((e = cub::DeviceScan::ExclusiveSum(cubtmp, tb, counts, first, (int)L.n_off, st)) != cudaSuccess) return cuda_fail(e, "scan first");
+  if (S->nnz > 0) {
+    tb = W.cub_bytes;
+    if ((e = cub::DeviceRadixSort::SortPairs(cubtmp, tb, ka, kb, va, vb, (int)S->nnz, 0, end_bit_for(L.n_off - 1), st)) != cudaSuccess)
+      return cuda_fail(e, "radix sort");
+    k_scatter<<<(unsigned)((S->nnz + 255) / 256), 256, 0, st>>>(kb, vb, S->nnz, off, first, sentinel_key, ids, vals);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_scatter");
+  }
+  knnjoin_index* h = new (std::nothrow) knnjoin_index();
+  if (!h) { set_error("host allocation failed"); return KNNJOIN_ERR_ARG; }
+  h->n_s = S->n_rows;
+  h->s_id_base = s_id_base;
+  h->d = d;
+  h->tile = tile;
+  h->n_tiles = L.n_tiles;
+  h->n_off = L.n_off;
+  h->unit_cap = L.unit_cap;
+  h->s_dtype = S->dtype;
+  h->off = off;
+  h->df = df;
+  h->ids = ids;
+  h->vals = vals;
+  h->storage_bytes = L.total;
+  *out = h;
+  return KNNJOIN_OK;
+}
+
+KJ_API knnjoin_status knnjoin_index_stats(const knnjoin_index* idx, knnjoin_index_info* out) {
+  if (!idx || !out) { set_error("NULL argument"); return KNNJOIN_ERR_ARG; }
+  out->n_s = idx->n_s;
+  out->s_id_base = idx->s_id_base;
+  out->d = idx->d;
+  out->tile = idx->tile;
+  out->n_tiles = idx->n_tiles;
+  out->offsets = idx->n_off;
+  out->unit_capacity = idx->unit_cap;
+  out->storage_bytes = (int64_t)idx->storage_bytes;
+  out->s_dtype = idx->s_dtype;
+  return KNNJOIN_OK;
+}
+
+KJ_API void knnjoin_free_index(knnjoin_index* idx) { delete idx; }

@@ -1,0 +1,160 @@
+// merge.cu -- K4 (S-sharded merge of partial top-k lists), CSR validation, error plumbing.
+//
+// K4: with S split into P contiguous id ranges (one per GPU), every rank computes the
+// top-k of every r against its shard (knnjoin_query -> out_keys); after an all-gather the P sorted lists
+// of a row are merged here.  Keys pack (score, lower id wins) into one unsigned integer
+// (topk.cuh), so the merge is exact and equals the single-index result bit for bit.  The fixed-point
+// scale of a row depends only on r and the dtype of S, so all ranks produce comparable keys.
+#include <cstdarg>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+#include "topk.cuh"
+
+namespace kj {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+knnjoin_status cuda_fail(cudaError_t e, const char* what) {
+  set_error("CUDA error in %s: %s", what, cudaGetErrorString(e));
+  return KNNJOIN_ERR_CUDA;
+}
+
+int ks_for_k(int32_t k) { return k <= 32 ? 1 : (k <= 128 ? 4 : 8); }
+
+__device__ unsigned long long g_bad;  // validation result word (module global, not an allocation)
+
+namespace {
+
+template <int KS>
+__global__ void k_merge(const uint64_t* __restrict__ keys, int32_t P, int64_t n, int32_t k,
+                        const double* __restrict__ inv_sigma, uint64_t* out_keys, int32_t* out_ids,
+                        float* out_scores) {
+  int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (r >= n) return;
+  uint64_t M[KS];
+#pragma unroll
+  for (int s = 0; s < KS; ++s) M[s] = 0;
+  uint64_t th = kKeyFloor;
+  for (int pr = 0; pr < P; ++pr) {
+    const uint64_t* src = keys + ((size_t)pr * n + r) * k;
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+      int pos = s * 32 + lane;
+      uint64_t c = pos < k ? src[pos] : 0;
+      list_offer_lanes<KS>(M, c, th, k, lane);
+    }
+  }
+  list_finalize<KS>(M, k, r, inv_sigma[r], out_keys, out_ids, out_scores, lane);
+}
+
+// warp per row; records the smallest offending row in *bad (as unsigned long long)
+__global__ void k_validate(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                           const void* __restrict__ values, knnjoin_dtype dt, int64_t n, int64_t nnz, int32_t d,
+                           unsigned long long* bad) {
+  int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  int64_t a = indptr[row], b = indptr[row + 1];
+  bool ok = (a <= b) && a >= 0 && b <= nnz;
+  if (row == 0 && a != 0) ok = false;
+  if (row == n - 1 && b != nnz) ok = false;
+  if (ok) {
+    for (int64_t j = a + lane; j < b; j += 32) {
+      int32_t f = indices[j];
+      if (f < 0 || f >= d) ok = false;
+      if (j > a && indices[j - 1] >= f) ok = false;
+      if (dt == KNNJOIN_INT8 && ((const int8_t*)values)[j] <= 0) ok = false;
+      if (dt == KNNJOIN_FP32) {
+        float v = ((const float*)values)[j];
+        if (!(v > 0.0f) || !isfinite(v)) ok = false;
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, !ok) && lane == 0) atomicMin(bad, (unsigned long long)row);
+}
+
+}  // namespace
+}  // namespace kj
+
+using namespace kj;
+
+KJ_API const char* knnjoin_last_error(void) { return g_err; }
+KJ_API const char* knnjoin_version(void) { return "knnjoin-b200 0.1 (sm_100a)"; }
+
+KJ_API size_t knnjoin_merge_workspace_bytes(const knnjoin_csr* R) {
+  if (!R || R->n_rows < 0) { set_error("bad R"); return 0; }
+  return align_up(8 * (size_t)R->n_rows, 256) + 256;
+}
+
+KJ_API knnjoin_status knnjoin_merge(const uint64_t* keys, int32_t P, const knnjoin_csr* R, int32_t d,
+                                    knnjoin_dtype s_dtype, int32_t k, uint64_t* out_keys, int32_t* out_ids, float* out_scores,
+                                    void* workspace, size_t workspace_bytes, void* stream) {
+  if (!R || P < 1 || k < 1 || k > kMaxK) { set_error("bad merge arguments (P %d, k %d)", P, k); return KNNJOIN_ERR_ARG; }
+  if (!out_keys && !out_ids && !out_scores) { set_error("no output"); return KNNJOIN_ERR_ARG; }
+  if (s_dtype != KNNJOIN_BINARY && s_dtype != KNNJOIN_INT8) { set_error("S dtype must be BINARY or INT8"); return KNNJOIN_ERR_UNSUPPORTED; }
+  size_t need = knnjoin_merge_workspace_bytes(R);
+  if (!workspace || workspace_bytes < need) { set_error("merge workspace %zu < %zu", workspace_bytes, need); return KNNJOIN_ERR_WORKSPACE; }
+  if (R->n_rows == 0) return KNNJOIN_OK;
+  if (!keys) { set_error("keys is NULL"); return KNNJOIN_ERR_ARG; }
+  cudaStream_t st = (cudaStream_t)stream;
+  double* inv = (double*)workspace;
+  if (d <= 0) { set_error("d must be > 0"); return KNNJOIN_ERR_DIM; }
+  launch_row_scale(R, d, s_dtype == KNNJOIN_INT8 ? 127 : 1, nullptr, inv, st);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "row scale");
+  int64_t threads = R->n_rows * 32;
+  unsigned grid = (unsigned)((threads + 255) / 256);
+  switch (ks_for_k(k)) {
+    case 1: k_merge<1><<<grid, 256, 0, st>>>(keys, P, R->n_rows, k, inv, out_keys, out_ids, out_scores); break;
+    case 4: k_merge<4><<<grid, 256, 0, st>>>(keys, P, R->n_rows, k, inv, out_keys, out_ids, out_scores); break;
+    default: k_merge<8><<<grid, 256, 0, st>>>(keys, P, R->n_rows, k, inv, out_keys, out_ids, out_scores); break;
+  }
+  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_merge");
+  return KNNJOIN_OK;
+}
+
+static std::mutex g_validate_mu;
+
+KJ_API knnjoin_status knnjoin_validate_csr(const knnjoin_csr* m, int32_t d, void* stream, int64_t* bad_row) {
+  if (bad_row) *bad_row = -1;
+  if (!m) { set_error("NULL csr"); return KNNJOIN_ERR_ARG; }
+  if (d <= 0) { set_error("d must be > 0"); return KNNJOIN_ERR_DIM; }
+  if (m->n_rows < 0 || m->nnz < 0) { set_error("negative sizes"); return KNNJOIN_ERR_CSR; }
+  if (m->n_rows == 0) {
+    if (m->nnz != 0) { set_error("n_rows == 0 but nnz != 0"); return KNNJOIN_ERR_CSR; }
+    return KNNJOIN_OK;
+  }
+  if (!m->indptr || (m->nnz > 0 && !m->indices)) { set_error("NULL pointers"); return KNNJOIN_ERR_ARG; }
+  if (m->dtype != KNNJOIN_BINARY && m->nnz > 0 && !m->values) { set_error("values missing for dtype %d", (int)m->dtype); return KNNJOIN_ERR_ARG; }
+  std::lock_guard<std::mutex> lock(g_validate_mu);  // g_bad is one module-global word
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long init = ~0ull, hbad = ~0ull;
+  cudaError_t e = cudaMemcpyToSymbolAsync(g_bad, &init, sizeof(init), 0, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "validate init");
+  unsigned long long* dbad = nullptr;
+  if ((e = cudaGetSymbolAddress((void**)&dbad, g_bad)) != cudaSuccess) return cuda_fail(e, "validate symbol");
+  int64_t threads = m->n_rows * 32;
+  k_validate<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(m->indptr, m->indices, m->values, m->dtype, m->n_rows,
+                                                             m->nnz, d, dbad);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "k_validate");
+  if ((e = cudaMemcpyFromSymbolAsync(&hbad, g_bad, sizeof(hbad), 0, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    return cuda_fail(e, "validate readback");
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "validate sync");
+  if (hbad != ~0ull) {
+    if (bad_row) *bad_row = (int64_t)hbad;
+    set_error("invalid CSR row %lld", (long long)hbad);
+    return KNNJOIN_ERR_CSR;
+  }
+  return KNNJOIN_OK;
+}

@@ -1,0 +1,54 @@
+"""-m "not gpu": the C-ABI library loads and exports every symbol include/knnjoin.h declares; host-only
+size queries and argument errors behave as documented (no device access)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "knnjoin.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(knnjoin_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_the_survey_entry_points():
+    names = _declared()
+    for n in ["knnjoin_build_index", "knnjoin_query", "knnjoin_merge", "knnjoin_validate_csr", "knnjoin_index_bytes",
+              "knnjoin_build_workspace_bytes", "knnjoin_query_workspace_bytes", "knnjoin_free_index",
+              "knnjoin_last_error", "knnjoin_index_stats"]:
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_1011_2807_b200 as kj
+    lib = ctypes.CDLL(kj.library_path())
+    for n in _declared():
+        assert hasattr(lib, n), n
+    assert "sm_100a" in kj.knnjoin_version()
+
+
+def test_index_bytes_host_only():
+    import paper_1011_2807_b200._binding as b
+    L = b._lib
+    S = b._CSR(100_000, 4_000_000, 0, 0, 0, b.BINARY)
+    opt = b._Options(8192, 0, 0.0)
+    n = L.knnjoin_index_bytes(ctypes.byref(S), 10_000, ctypes.byref(opt))
+    nt = (100_000 + 8191) // 8192
+    n_off = 10_000 * (nt + 1) + 1
+    cap = 4_000_000 // 8 + min(4_000_000, 10_000 * nt) + 1
+    al = lambda x: (x + 255) // 256 * 256
+    assert n == al(al(al(4 * n_off) + 4 * 10_000) + 16 * cap)
+
+
+@pytest.mark.parametrize("d,tile,dtype,msg", [(0, 8192, 0, "d must be"), (100, 1000, 0, "tile"), (100, 8192, 2, "dtype")])
+def test_build_argument_errors(d, tile, dtype, msg):
+    import paper_1011_2807_b200._binding as b
+    L = b._lib
+    S = b._CSR(10, 20, 0, 0, 0, dtype)
+    opt = b._Options(tile, 0, 0.0)
+    assert L.knnjoin_index_bytes(ctypes.byref(S), d, ctypes.byref(opt)) == 0
+    assert msg in b.knnjoin_last_error()

@@ -1,0 +1,188 @@
+"""-m gpu: the CUDA path (through the C ABI) against the oracle, element by element."""
+import numpy as np
+import pytest
+import torch
+
+import gen
+import oracle
+from tests.gpu_util import assert_parity, gpu_join
+from tests.util import csr_from_rows, random_csr
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(R, S, k, tile=0, batch_rows=0, threads=8, **kw):
+    g_ids, g_sc = gpu_join(R, S, k, tile=tile, batch_rows=batch_rows, **kw)
+    o_ids, o_sc = oracle.knn(R, S, k, threads=threads)
+    assert_parity(R, S, g_ids, g_sc, o_ids, o_sc)
+    return g_ids, g_sc
+
+
+def test_hand_example():
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "hand_example.json")))
+    R = csr_from_rows(g["R"], g["d"], "binary")
+    S = csr_from_rows(g["S"], g["d"], "binary")
+    for k, want in g["expect"].items():
+        ids, sc = gpu_join(R, S, int(k), tile=2048)
+        assert [[int(a), int(b)] for a, b in zip(ids[0], sc[0])] == want
+
+
+@pytest.mark.parametrize("dtr,dts", [("binary", "binary"), ("int8", "int8"), ("fp32", "binary"), ("int8", "binary"),
+                                     ("binary", "int8"), ("fp32", "int8")])
+@pytest.mark.parametrize("k", [1, 5, 33, 256])
+def test_random_small_multi_tile(dtr, dts, k):
+    """Several tiles (tile=2048) with a ragged tail, tie-heavy small value ranges."""
+    rng = np.random.default_rng(abs(hash((dtr, dts, k))) % 2**32)
+    d = 300
+    R = random_csr(rng, 37, d, 0, 40, dtr, vmax=4)
+    S = random_csr(rng, 5000, d, 0, 30, dts, vmax=4)
+    _check(R, S, k, tile=2048)
+
+
+@pytest.mark.parametrize("batch_rows", [1, 2, 4, 6, 8])
+def test_batch_sizes(batch_rows):
+    rng = np.random.default_rng(batch_rows)
+    R = random_csr(rng, 53, 200, 1, 50, "fp32")
+    S = random_csr(rng, 9000, 200, 1, 30, "binary")
+    _check(R, S, 10, tile=4096, batch_rows=batch_rows)
+
+
+def test_edge_cases():
+    d = 64
+    R = csr_from_rows([[0, 1, 2], [], [63], [5, 6]], d, "binary")
+    S = csr_from_rows([[0], [], [1, 2, 3], [63], [7]], d, "binary")
+    _check(R, S, 4, tile=2048)
+    # k larger than #positives everywhere; k = 1
+    _check(R, S, 7, tile=2048)
+    _check(R, S, 1, tile=2048)
+    # R features beyond d are ignored (S cannot have them)
+    Rw = csr_from_rows([[0, 70, 80]], 128, "binary")
+    Sw = csr_from_rows([[0], [0, 1]], 128, "binary")
+    ids, sc = gpu_join(Rw, Sw, 2, d=64, tile=2048)
+    assert ids.tolist() == [[0, 1]] and sc.tolist() == [[1.0, 1.0]]
+
+
+def test_empty_inputs():
+    import paper_1011_2807_b200 as kj
+    d = 32
+    R = csr_from_rows([[1, 2], [3]], d, "binary")
+    Sempty = csr_from_rows([], d, "binary")
+    ids, sc = gpu_join(R, Sempty, 3, tile=2048)
+    assert (ids == -1).all() and (sc == 0).all()
+    Rempty = csr_from_rows([], d, "binary")
+    S = csr_from_rows([[1]], d, "binary")
+    ids, sc = gpu_join(Rempty, S, 3, tile=2048)
+    assert ids.shape == (0, 3)
+
+
+def test_counters_match_eq4():
+    """Unpruned postings visited == Eq. 4 second term = sum_d n_R(d) n_S(d), exactly."""
+    c = gen.CONFIGS["C2"].scaled(300, 20000)
+    R, S = gen.generate(c, "R"), gen.generate(c, "S")
+    cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+    gpu_join(R, S, c.k, counters=cnt)
+    nR = np.bincount(R.indices, minlength=c.d)
+    nS = np.bincount(S.indices, minlength=c.d)
+    assert int(cnt[0]) == int((nR.astype(np.int64) * nS).sum())
+    assert int(cnt[1]) > 0
+
+
+def test_deterministic():
+    c = gen.CONFIGS["C3"].scaled(200, 40000)
+    R, S = gen.generate(c, "R"), gen.generate(c, "S")
+    a = gpu_join(R, S, c.k)
+    b = gpu_join(R, S, c.k, batch_rows=2)
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_array_equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("name,n_r,n_s,tile", [
+    ("C1", None, None, 0),          # full C1 (configs[0]): bit-exact
+    ("C1", None, None, 2048),
+    ("C2", 400, 30000, 0),
+    ("C3", 300, 50000, 0),
+    ("C4", 200, 40000, 0),
+    ("C5", 60, 30000, 0),           # int8 x int8, k=100: bit-exact
+    ("C5", 40, 20000, 4096),
+])
+def test_configs_scaled(name, n_r, n_s, tile):
+    c = gen.CONFIGS[name].scaled(n_r, n_s)
+    R, S = gen.generate(c, "R"), gen.generate(c, "S")
+    _check(R, S, c.k, tile=tile)
+
+
+def test_sharded_merge_equals_single_index():
+    """T7: S split in P contiguous shards, P indexes with s_id_base, knnjoin_merge == one index, bit-exact."""
+    import paper_1011_2807_b200 as kj
+    c = gen.CONFIGS["C2"].scaled(150, 30000)
+    R, S = gen.generate(c, "R"), gen.generate(c, "S")
+    full_ids, full_sc, full_keys = gpu_join(R, S, c.k, want_keys=True)
+    for P in (2, 3, 4):
+        bounds = np.linspace(0, S.n_rows, P + 1).astype(np.int64)
+        keys = []
+        for p in range(P):
+            part = S.take_rows(np.arange(bounds[p], bounds[p + 1]))
+            _, _, kk = gpu_join(R, part, c.k, d=c.d, s_id_base=int(bounds[p]), want_keys=True)
+            keys.append(torch.from_numpy(kk))
+        allk = torch.stack(keys).cuda()
+        dR = kj.DeviceCSR.from_host(R)
+        ids, sc, mk = kj.knnjoin_merge(allk, dR, c.d, kj.BINARY, c.k, want_keys=True)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(ids.cpu().numpy(), full_ids)
+        np.testing.assert_array_equal(sc.cpu().numpy(), full_sc.astype(np.float32))
+        np.testing.assert_array_equal(mk.cpu().numpy(), full_keys)
+
+
+def test_validate_csr():
+    import paper_1011_2807_b200 as kj
+    ok = kj.DeviceCSR.from_arrays(np.array([0, 2, 3]), np.array([1, 4, 0]), np.array([1.0, 2.0, 3.0], np.float32))
+    assert kj.knnjoin_validate_csr(ok, 8) == (0, -1)
+    bad = kj.DeviceCSR.from_arrays(np.array([0, 2, 3]), np.array([4, 1, 0]), np.array([1.0, 2.0, 3.0], np.float32))
+    assert kj.knnjoin_validate_csr(bad, 8) == (3, 0)
+    neg = kj.DeviceCSR.from_arrays(np.array([0, 2, 3]), np.array([1, 4, 0]), np.array([1.0, 2.0, -3.0], np.float32))
+    assert kj.knnjoin_validate_csr(neg, 8) == (3, 1)
+    oob = kj.DeviceCSR.from_arrays(np.array([0, 1, 2]), np.array([1, 9]))
+    assert kj.knnjoin_validate_csr(oob, 8) == (3, 1)
+
+
+def test_index_layout_matches_scipy_csc():
+    """T3: decode the built index (slices per (feature, tile)) and compare with scipy's CSC per tile."""
+    import scipy.sparse as sp
+    import paper_1011_2807_b200 as kj
+    c = gen.CONFIGS["C5"].scaled(10, 9000)
+    S = gen.generate(c, "S")
+    T = 4096
+    dS = kj.DeviceCSR.from_host(S)
+    idx = kj.knnjoin_build_index(dS, c.d, tile=T)
+    torch.cuda.synchronize()
+    st = kj.knnjoin_index_stats(idx)
+    raw = idx.storage.cpu().numpy()
+    NT = st["n_tiles"]
+    n_off = st["offsets"]
+    off = raw[:4 * n_off].view(np.uint32)
+    al = lambda x: (x + 255) // 256 * 256
+    df_at = al(4 * n_off)
+    df = raw[df_at:df_at + 4 * c.d].view(np.int32)
+    ids_at = al(df_at + 4 * c.d)
+    cap = st["unit_capacity"]
+    ids = raw[ids_at:ids_at + 16 * cap].view(np.uint16)
+    vals_at = al(ids_at + 16 * cap)
+    vals = raw[vals_at:vals_at + 8 * cap].view(np.uint8)
+    np.testing.assert_array_equal(df, np.bincount(S.indices, minlength=c.d))
+    M = sp.csr_matrix((S.values.astype(np.int64), S.indices, S.indptr), shape=(S.n_rows, c.d)).tocsc()
+    rng = np.random.default_rng(0)
+    for f in rng.choice(c.d, 300, replace=False):
+        col = M[:, f]
+        rows_f = col.indices
+        vals_f = col.data
+        for t in range(NT):
+            a, b = off[f * (NT + 1) + t], off[f * (NT + 1) + t + 1]
+            got_ids = ids[8 * a:8 * b]
+            got_vals = vals[8 * a:8 * b]
+            keep = got_ids != 0xFFFF
+            order = np.argsort(got_ids[keep])
+            sel = (rows_f >= t * T) & (rows_f < (t + 1) * T)
+            np.testing.assert_array_equal(got_ids[keep][order].astype(np.int64), rows_f[sel] - t * T)
+            np.testing.assert_array_equal(got_vals[keep][order], vals_f[sel])
+            assert b - a == (sel.sum() + 7) // 8
