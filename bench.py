@@ -1,0 +1,403 @@
+"""bench.py -- |R|·|S| pairs/s of the B200 sparse KNN-join hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+
+A step is one pass of the whole hot path over the config's synthetic input:
+knnjoin_build_index(S) + knnjoin_query(R, k) -> ids + scores, inputs already resident in HBM.  L2 is
+flushed (256 MiB write) before every timed step, outside the step's event pair.  N>1 (torchrun, one rank
+per GPU, NCCL): weak scaling -- every rank owns its own |S|-row shard of an N·|S|-row S (rows
+[p|S|, (p+1)|S|) of the same counter-based generator), R is replicated, each rank's top-k keys are
+all-gathered (NCCL over NVLink) and merged (K4); value = N·|R|·|S| / max-over-ranks time.
+
+--impl reference times the CPU oracle (oracle/, the plain brute-force definition) on the host cores, on a
+bounded row sample of the same workload per step (rank 0 only under torchrun).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import gen  # noqa: E402
+
+METRIC = "KNN-join |R|·|S| pairs/s and achieved HBM GB/s fraction at 1/2/4/8 B200"
+FALLBACK_HBM_GBS = 6650.0
+BAD_REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2", choices=sorted(gen.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--tile", type=int, default=0)
+    ap.add_argument("--batch-rows", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_desc(cfg, world):
+    r, s = cfg.R, cfg.S
+    law = {gen.UNIFORM: "uniform", gen.ZIPF: "Zipf", gen.BANDS: "5 Gaussian bands"}
+    return (f"{cfg.name}: |R|={r.n_rows} {gen.VALUE_DTYPE[r.value_law]} x |S|={s.n_rows * world}"
+            f"{' (' + str(world) + ' shards of ' + str(s.n_rows) + ')' if world > 1 else ''} "
+            f"{gen.VALUE_DTYPE[s.value_law]}, d={cfg.d}, {law[s.feat_law]} features, k={cfg.k}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the timed region."""
+
+    FIELDS = ["index", "clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self._t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def recorded_traffic(cfg_name: str):
+    """dram bytes per launch of the accumulate kernel from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(cfg_name)
+    except Exception:
+        return None
+
+
+def visits_and_bytes(R, S, d):
+    nR = np.bincount(R.indices[R.indices < d], minlength=d).astype(np.int64)
+    nS = np.bincount(S.indices, minlength=d).astype(np.int64)
+    V = int((nR * nS).sum())
+    b_post = 2 if S.values is None else 3
+    return V, b_post
+
+
+# ------------------------------------------------------------------------------------ CPU oracle leg
+def run_oracle_sample(cfg, R, S, rows, threads):
+    import oracle
+    t0 = time.perf_counter()
+    oracle.knn(R, S, cfg.k, rows=rows, threads=threads)
+    return time.perf_counter() - t0
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(cfg, R, S, budget_s=15.0):
+    """The oracle, as it stands, on a bounded row sample of the same workload, rows split over host threads."""
+    cores = host_cores()
+    rng = np.random.default_rng(1234)
+    probe = rng.choice(R.n_rows, size=min(R.n_rows, cores), replace=False)
+    t = run_oracle_sample(cfg, R, S, probe, cores)
+    per_row = t / max(len(probe), 1) * cores  # seconds per row per thread
+    n_rows = int(max(cores, min(R.n_rows, budget_s * cores / max(per_row, 1e-9))))
+    rows = rng.choice(R.n_rows, size=n_rows, replace=False)
+    t = run_oracle_sample(cfg, R, S, rows, cores)
+    pairs = n_rows * S.n_rows
+    return {"value": pairs / t, "unit": "pairs/s", "cores": cores, "kind": "oracle",
+            "sample": f"{n_rows} random rows of R x all {S.n_rows} rows of S ({pairs:.3e} pairs, {t:.1f} s), "
+                      f"single-threaded C oracle per thread, rows split over {cores} host threads"}
+
+
+def bench_reference(args):
+    rank, world, _ = dist_env()
+    cfg = gen.CONFIGS[args.config]
+    if rank != 0:
+        return
+    R, S = gen.generate(cfg, "R"), gen.generate(cfg, "S", 0, cfg.S.n_rows)
+    cores = host_cores()
+    rng = np.random.default_rng(99)
+    probe = rng.choice(R.n_rows, size=min(R.n_rows, cores), replace=False)
+    t = run_oracle_sample(cfg, R, S, probe, cores)
+    per_row = t / len(probe) * cores
+    total_budget = 120.0
+    steps = args.steps + args.warmup
+    rows_per_step = int(max(cores, min(R.n_rows, total_budget / steps * cores / max(per_row, 1e-9))))
+    times = []
+    for i in range(steps):
+        rows = rng.choice(R.n_rows, size=rows_per_step, replace=False)
+        dt = run_oracle_sample(cfg, R, S, rows, cores)
+        if i >= args.warmup:
+            times.append(dt)
+    pairs = rows_per_step * S.n_rows
+    value = pairs * len(times) / sum(times)
+    sample = (f"per step {rows_per_step} random rows of R x all {S.n_rows} rows of S ({pairs:.3e} pairs); "
+              f"oracle rows split over {cores} host threads")
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": workload_desc(cfg, 1), "k": cfg.k, "seed": cfg.seed},
+           "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------------------------------ GPU leg
+def bench_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1011_2807_b200 as kj
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = gen.CONFIGS[args.config]
+    n_s = cfg.S.n_rows
+    big = cfg.scaled(None, n_s * world)
+    R = gen.generate(big, "R")
+    S = gen.generate(big, "S", rank * n_s, n_s)
+    s_base = rank * n_s
+    d, k = cfg.d, cfg.k
+    V, b_post = visits_and_bytes(R, S, d)
+
+    stream = torch.cuda.current_stream()
+    dR = kj.DeviceCSR.from_host(R, dev)
+    dS = kj.DeviceCSR.from_host(S, dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step(dS_, dR_, kernel_events=None):
+        idx = kj.knnjoin_build_index(dS_, d, s_id_base=s_base, tile=args.tile)
+        if world == 1:
+            ids, sc, _ = kj.knnjoin_query(idx, dR_, k, batch_rows=args.batch_rows, events=kernel_events)
+            return ids, sc
+        _, _, keys = kj.knnjoin_query(idx, dR_, k, want_keys=True, want_ids=False, batch_rows=args.batch_rows,
+                                      events=kernel_events)
+        gathered = torch.empty((world,) + tuple(keys.shape), dtype=keys.dtype, device=dev)
+        dist.all_gather_into_tensor(gathered, keys)
+        ids, sc, _ = kj.knnjoin_merge(gathered, dR_, d, dS_.dtype, k)
+        return ids, sc
+
+    for _ in range(args.warmup):
+        step(dS, dR)
+    torch.cuda.synchronize()
+
+    # launch count of our kernels per step (one untimed profiled step; never inside the timed region)
+    launches_per_step = None
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step(dS, dR)
+            torch.cuda.synchronize()
+        names = [e.name for e in prof.events() if e.device_type.name == "CUDA"]
+        ours = [n for n in names if ("kj::" in n or "cub::" in n) and "Memset" not in n and "Memcpy" not in n]
+        launches_per_step = len(ours)
+    except Exception:
+        launches_per_step = None
+
+    def timed_region():
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        kb = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        ke = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        for ev in kb + ke:  # materialise the cudaEvent handles; the library re-records them around its kernel
+            ev.record(stream)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        sampler = ClockSampler(local)
+        sampler.start()
+        time.sleep(0.05)
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)  # > L2 (126 MB): evict the previous step's index and inputs
+            starts[i].record(stream)
+            step(dS, dR, (kb[i], ke[i]))
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clocks = sampler.stop()
+        step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+        kern_ms = [s.elapsed_time(e) for s, e in zip(kb, ke)]
+        return step_ms, kern_ms, clocks
+
+    step_ms, kern_ms, clocks = timed_region()
+    if any(r in BAD_REASONS for r in clocks.get("reasons", [])):
+        step_ms, kern_ms, clocks = timed_region()  # rejected: re-measure once
+        clocks["remeasured"] = True
+    total_ms = sum(step_ms)
+    kern_avg = sum(kern_ms) / len(kern_ms)
+    t = torch.tensor([total_ms, kern_avg], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, kern_avg_max = float(t[0]), float(t[1])
+    ms_per_step = total_ms / args.steps
+    pairs_per_step = R.n_rows * n_s * world
+    value = pairs_per_step / (ms_per_step * 1e-3)
+
+    # end to end: pinned host CSR -> device, build + query (+ gather/merge), result -> pinned host
+    e2e = None
+    if not args.no_e2e:
+        import torch as _t
+        hS = [_t.from_numpy(x).pin_memory() if x is not None else None for x in (S.indptr, S.indices, S.values)]
+        hR = [_t.from_numpy(x).pin_memory() if x is not None else None for x in (R.indptr, R.indices, R.values)]
+        h2d = sum(x.numel() * x.element_size() for x in hS + hR if x is not None)
+        out_ids = _t.empty((R.n_rows, k), dtype=_t.int32).pin_memory()
+        out_sc = _t.empty((R.n_rows, k), dtype=_t.float32).pin_memory()
+        d2h = out_ids.numel() * 4 + out_sc.numel() * 4
+
+        def e2e_step():
+            dS2 = kj.DeviceCSR.from_arrays(hS[0], hS[1], hS[2], dev, non_blocking=True)
+            dR2 = kj.DeviceCSR.from_arrays(hR[0], hR[1], hR[2], dev, non_blocking=True)
+            ids, sc = step(dS2, dR2)
+            out_ids.copy_(ids, non_blocking=True)
+            out_sc.copy_(sc, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        n_e2e = max(3, min(args.steps, 20))
+        if world > 1:
+            dist.barrier()
+        es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tot = 0.0
+        for i in range(n_e2e):
+            flush.fill_(i & 0xFF)
+            es.record(stream)
+            e2e_step()
+            ee.record(stream)
+            ee.synchronize()
+            tot += es.elapsed_time(ee)
+        tt = torch.tensor([tot / n_e2e], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": pairs_per_step / (float(tt[0]) * 1e-3), "unit": "pairs/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": float(tt[0]), "steps": n_e2e,
+               "path": "pinned host CSR -> cudaMemcpyAsync -> knnjoin_build_index + knnjoin_query"
+                       + (" + NCCL all-gather + knnjoin_merge" if world > 1 else "") + " -> pinned host ids/scores"}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = measured_peak()
+    achieved = V * b_post / (kern_avg_max * 1e-3) / 1e9
+    stats = kj.knnjoin_index_stats(kj.knnjoin_build_index(dS, d, s_id_base=s_base, tile=args.tile))
+    props = torch.cuda.get_device_properties(dev)
+    out = {
+        "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "i32", "data": "synthetic",
+        "config": {"workload": workload_desc(cfg, world), "k": k, "d": d, "seed": cfg.seed,
+                   "R_rows": R.n_rows, "S_rows_per_gpu": n_s, "S_rows_total": n_s * world,
+                   "nnz_R": int(R.nnz), "nnz_S_per_gpu": int(S.nnz), "tile": stats["tile"],
+                   "n_tiles": stats["n_tiles"], "batch_rows": args.batch_rows or "auto",
+                   "step": "knnjoin_build_index(S) + knnjoin_query(R,k)" + (" + all_gather + knnjoin_merge" if world > 1 else ""),
+                   "l2": "flushed before every timed step (256 MiB write, outside the step's events)",
+                   "parallelism": f"S-sharded x{world}" if world > 1 else "1 GPU",
+                   "sms": props.multi_processor_count, "l2_bytes": getattr(props, "L2_cache_size", None)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": recorded_traffic(cfg.name),
+                     "kernel": "k_accumulate_topk", "kernel_ms": kern_avg_max,
+                     "algorithmic_bytes": V * b_post, "visits": V, "bytes_per_visit": b_post,
+                     "peak_source": peak_src,
+                     "note": "algorithmic posting bytes (V x B_post, SURVEY.md §8(d)); slices are re-read from L2 "
+                             "across rows, so logical GB/s can exceed HBM peak"},
+        "clocks": clocks,
+        "gpu_launches": (launches_per_step * args.steps) if launches_per_step is not None else None,
+        "breakdown": {"kernel_ms": kern_avg_max, "step_ms": ms_per_step,
+                      "other_ms": ms_per_step - kern_avg_max, "launches_per_step": launches_per_step},
+    }
+    if e2e is not None:
+        out["e2e"] = e2e
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(cfg, R, S)
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -212,6 +212,8 @@ def knnjoin_query(index: Index, R: DeviceCSR, k: int, want_keys: bool = False, w
                   workspace: torch.Tensor | None = None):
     """Returns (ids int32 [n,k], scores float32 [n,k], keys uint64-as-int64 [n,k] or None)."""
     cR = R._c()
+    if events and (events[0].cuda_event == 0 or events[1].cuda_event == 0):
+        raise ValueError("timing events must have been recorded once (so their cudaEvent handles exist)")
     qo = _QueryOptions(batch_rows, counters.data_ptr() if counters is not None else 0,
                        events[0].cuda_event if events else 0, events[1].cuda_event if events else 0)
     wbytes = _lib.knnjoin_query_workspace_bytes(index.handle, ctypes.byref(cR), k, ctypes.byref(qo))

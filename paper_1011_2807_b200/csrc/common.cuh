@@ -18,9 +18,9 @@ constexpr int kThreads = kWarps * 32;  // 512
 constexpr int kCap = kThreads;         // posting runs staged in shared memory per chunk (one per thread)
 constexpr int kMaxK = 256;
 constexpr int kDefaultTile = 8192;
-constexpr int kMaxTile = 32768;        // local ids are 15-bit; 0xFFFF is the padding sentinel
+constexpr int kMaxTile = 32768;        // local ids < tile; padding ids are tile + (0..31) (dummy columns)
 constexpr int kTileQuantum = 2048;     // tile must split into kWarps column strips of 128-column chunks
-constexpr uint16_t kSentinel = 0xFFFF;
+constexpr int kPadCols = 32;           // dummy score columns per row that absorb padding postings
 constexpr uint64_t kKeyFloor = 0x00000000FFFFFFFFull;  // score 0 with every id: admits nothing
 constexpr double kFixedOne = 1073741824.0;              // 2^30: per-row fixed-point scale numerator
 
@@ -54,7 +54,7 @@ struct knnjoin_index {
   knnjoin_dtype s_dtype = KNNJOIN_BINARY;
   const uint32_t* off = nullptr;  // [n_off] posting-unit (16 B) offsets, feature-major: f*(n_tiles+1)+t
   const int32_t* df = nullptr;    // [d] |I_d| (document frequency of each feature in S)
-  const uint16_t* ids = nullptr;  // [unit_cap*8] 15-bit local S ids, 0xFFFF padding
+  const uint16_t* ids = nullptr;  // [unit_cap*8] local S ids (< tile); padding = tile + (u mod 32)
   const uint8_t* vals = nullptr;  // [unit_cap*8] INT8 S weights (nullptr for BINARY S)
   size_t storage_bytes = 0;
 };

@@ -6,7 +6,8 @@
 // and laid out feature-major so that slice (f, t) = I_f ∩ tile t is contiguous:
 //
 //   off[f*(n_tiles+1) + t] .. off[f*(n_tiles+1) + t + 1]   16-byte posting units of slice (f, t)
-//   ids[8*u .. 8*u+8)                                        8 local ids (s - t*tile) per unit, 0xFFFF pad
+//   ids[8*u .. 8*u+8)                                        8 local ids (s - t*tile) per unit; padding
+//                                                            entries hold tile + (u mod 32), a dummy column
 //   vals[8*u .. 8*u+8)                                       INT8 S weights (same positions)
 //
 // Steps (all stream-ordered, integer, deterministic):
@@ -134,6 +135,16 @@ __global__ void k_count(const int64_t* __restrict__ indptr, const int32_t* __res
   }
 }
 
+// padding entries point at one of 32 dummy score columns [tile, tile+32) (spread over banks by unit index),
+// so the accumulation kernel issues its shared-memory atomics without a per-posting predicate
+__global__ void k_fill_pads(uint4* __restrict__ ids, int64_t units, uint32_t tile) {
+  int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= units) return;
+  uint32_t pad = tile + (uint32_t)(u & 31);
+  pad |= pad << 16;
+  ids[u] = make_uint4(pad, pad, pad, pad);
+}
+
 __global__ void k_units(const uint32_t* __restrict__ counts, uint32_t* __restrict__ units, int64_t n) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) units[i] = (counts[i] + 7u) >> 3;
@@ -223,7 +234,8 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   cudaError_t e;
   if ((e = cudaMemsetAsync(counts, 0, 4 * (size_t)L.n_off, st)) != cudaSuccess) return cuda_fail(e, "memset counts");
   if ((e = cudaMemsetAsync(df, 0, 4 * (size_t)d, st)) != cudaSuccess) return cuda_fail(e, "memset df");
-  if ((e = cudaMemsetAsync(ids, 0xFF, 16 * (size_t)L.unit_cap, st)) != cudaSuccess) return cuda_fail(e, "memset ids");
+  k_fill_pads<<<(unsigned)((L.unit_cap + 255) / 256), 256, 0, st>>>((uint4*)ids, L.unit_cap, (uint32_t)tile);
+  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_fill_pads");
   if (vals && (e = cudaMemsetAsync(vals, 0, 8 * (size_t)L.unit_cap, st)) != cudaSuccess) return cuda_fail(e, "memset vals");
   if (S->n_rows > 0) {
     int64_t threads = S->n_rows * 32;

@@ -170,9 +170,12 @@ __device__ __forceinline__ uint64_t block_exclusive_scan_u64(uint64_t v, uint64_
 }
 
 // ------------------------------------------------------------------------------ a4 + a5 + a7 kernel
+// Score rows have stride T + kPadCols: columns [T, T+32) absorb padding postings (never scanned).
+__host__ __device__ inline int acc_stride(int T) { return T + kPadCols; }
+
 // the score array doubles as the scratch of the end-of-batch list merge ([kWarps][B][k] keys)
 __host__ __device__ inline size_t acc_region_bytes(int B, int T, int k) {
-  size_t a = (size_t)B * T * 4, m = (size_t)kWarps * B * k * 8;
+  size_t a = (size_t)B * acc_stride(T) * 4, m = (size_t)kWarps * B * k * 8;
   return align_up(a > m ? a : m, 16);
 }
 
@@ -192,11 +195,19 @@ struct Smem {
   }
 };
 
-template <int B, int KS>
+__device__ __forceinline__ void red_add_shared(uint32_t addr, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+constexpr int kWinChunk = 4;  // 32-unit windows a warp takes per grab of the dynamic window counter
+
+template <int B, int KS, bool SINT8>
 __global__ void __launch_bounds__(kThreads, 1) k_accumulate_topk(QP p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int T = p.T;
+  const int TS = acc_stride(T);
   uint32_t* acc = (uint32_t*)smem;
+  const uint32_t acc_s = (uint32_t)__cvta_generic_to_shared(acc);
   uint32_t* s_ustart = (uint32_t*)(smem + acc_region_bytes(B, T, p.k));
   uint32_t* s_P = s_ustart + kCap;
   uint32_t* s_fm = s_P + kCap + 1;
@@ -205,14 +216,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_accumulate_topk(QP p) {
                            (size_t)kCap * B * 4, 16);
   uint64_t* s_warp = (uint64_t*)(smem + at);
   uint64_t* s_theta = s_warp + kWarps;
-  int* s_misc = (int*)(s_theta + 8);
+  int* s_misc = (int*)(s_theta + 8);  // [0] batch, [1] n_items, [2] TOT, [3] window counter
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = p.k;
-  const bool wint8 = p.vals != nullptr;
+  constexpr bool wint8 = SINT8;
   unsigned long long n_visits = 0, n_inserts = 0;
 
-  for (int i = tid; i < B * T / 4; i += kThreads) ((uint4*)acc)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = tid; i < (int)(acc_region_bytes(B, T, k) / 16); i += kThreads) ((uint4*)acc)[i] = make_uint4(0, 0, 0, 0);
 
   for (;;) {
     __syncthreads();
@@ -264,6 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_accumulate_topk(QP p) {
           if (tid == 0) {
             s_misc[1] = (int)(total >> 32);
             s_misc[2] = (int)(uint32_t)total;
+            s_misc[3] = 0;
             s_P[(uint32_t)(total >> 32)] = (uint32_t)total;
           }
           __syncthreads();
@@ -273,12 +285,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_accumulate_topk(QP p) {
           const int n_items = s_misc[1];
           const uint32_t TOT = (uint32_t)s_misc[2];
           const uint32_t nwin = (TOT + 31) >> 5;
-          const uint32_t w0 = (uint32_t)(((uint64_t)warp * nwin) / kWarps);
-          const uint32_t w1 = (uint32_t)(((uint64_t)(warp + 1) * nwin) / kWarps);
-          if (w0 < w1) {
-            const uint32_t p_begin = w0 * 32, p_end = min(TOT, w1 * 32);
-            // largest e with P[e] <= p_begin
-            int lo = 0, hi = n_items - 1;
+          for (;;) {
+            uint32_t c = 0;
+            if (lane == 0) c = atomicAdd((unsigned*)&s_misc[3], (unsigned)kWinChunk);
+            c = __shfl_sync(0xffffffffu, c, 0);
+            if (c >= nwin) break;
+            const uint32_t p_begin = c * 32, p_end = min(TOT, (c + kWinChunk) * 32);
+            int lo = 0, hi = n_items - 1;  // largest e with P[e] <= p_begin
             while (lo < hi) {
               int mid = (lo + hi + 1) >> 1;
               if (s_P[mid] <= p_begin) lo = mid; else hi = mid - 1;
@@ -291,16 +304,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_accumulate_topk(QP p) {
                 const int j = min(e_cur + 1 + lane, n_items);
                 const uint32_t o = s_P[j];
                 const uint32_t pp = p0 + lane;
-                int c = 0;
+                int cc = 0;
 #pragma unroll
                 for (int st = 16; st; st >>= 1) {
-                  uint32_t v = __shfl_sync(0xffffffffu, o, c + st - 1);
-                  if (v <= pp) c += st;
+                  uint32_t v = __shfl_sync(0xffffffffu, o, cc + st - 1);
+                  if (v <= pp) cc += st;
                 }
-                e = e_cur + c;
+                e = e_cur + cc;
               }
               const uint32_t pp = p0 + lane;
               valid = pp < p_end;
+              if (!valid) e = e_cur;
               e_out = e;
               unit = s_ustart[e] + (pp - s_P[e]);
               const int e31 = __shfl_sync(0xffffffffu, e, 31);
@@ -311,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_accumulate_topk(QP p) {
             uint32_t uA;
             bool vA;
             lookup(p_begin, eA, uA, vA);
-            uint4 idA = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+            uint4 idA = make_uint4(0, 0, 0, 0);
             uint2 wA = make_uint2(0, 0);
             if (vA) {
               idA = ldg_nc_v4(p.ids + (size_t)uA * 8);
@@ -321,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_accumulate_topk(QP p) {
               int eB = 0;
               uint32_t uB = 0;
               bool vB = false;
-              uint4 idB = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+              uint4 idB = make_uint4(0, 0, 0, 0);
               uint2 wB = make_uint2(0, 0);
               if (p0 + 32 < p_end) {
                 lookup(p0 + 32, eB, uB, vB);
@@ -333,24 +347,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_accumulate_topk(QP p) {
               if (vA) {
                 const uint32_t mask = s_fm[eA] >> 24;
                 const uint32_t wd[4] = {idA.x, idA.y, idA.z, idA.w};
+                uint32_t off4[8], w8[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  off4[j] = ((wd[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu) * 4u;
+                  w8[j] = wint8 ? (((j < 4 ? wA.x : wA.y) >> (8 * (j & 3))) & 0xFFu) : 1u;
+                }
 #pragma unroll
                 for (int b = 0; b < B; ++b) {
                   if (mask & (1u << b)) {
                     const uint32_t q = (uint32_t)s_q[eA * B + b];
-                    uint32_t* row = acc + (size_t)b * T;
+                    const uint32_t rb = acc_s + (uint32_t)(b * TS * 4);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                      const uint32_t id = (wd[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu;
-                      uint32_t add = q;
-                      if (wint8) add = q * ((j < 4 ? (wA.x >> (8 * j)) : (wA.y >> (8 * (j - 4)))) & 0xFFu);
-                      if (id != 0xFFFFu) atomicAdd(row + id, add);
+                      red_add_shared(rb + off4[j], wint8 ? q * w8[j] : q);
                     }
                   }
                 }
                 if (p.counters) {
                   int nid = 0;
 #pragma unroll
-                  for (int j = 0; j < 8; ++j) nid += ((wd[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu) != 0xFFFFu;
+                  for (int j = 0; j < 8; ++j) nid += off4[j] < (uint32_t)T * 4u;
                   n_visits += (unsigned long long)nid * __popc(mask);
                 }
               }
@@ -373,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_accumulate_topk(QP p) {
               const uint64_t sh = *(volatile uint64_t*)&s_theta[b];
               if (sh > th) th = sh;
             }
-            uint32_t* row = acc + (size_t)b * T;
+            uint32_t* row = acc + (size_t)b * TS;
             for (int c = 0; c < cols; c += 128) {
               const int col = cbase + c + lane * 4;
               uint4 v = *(uint4*)(row + col);
@@ -410,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_accumulate_topk(QP p) {
     }
     // ---------------------------------------------------------------------- merge lists + finalize (a7)
     {
-      uint64_t* scratch = (uint64_t*)acc;  // [kWarps][B][k]; acc is all-zero here
+      uint64_t* scratch = (uint64_t*)acc;  // [kWarps][B][k]; acc columns < T are all zero here
 #pragma unroll
       for (int b = 0; b < B; ++b)
 #pragma unroll
@@ -491,13 +508,18 @@ bool query_ws_layout(int64_t n_r, int64_t nnz_r, int B, QueryWs* W) {
   return true;
 }
 
+template <int B, int KS, bool SINT8>
+cudaError_t launch_main3(const QP& p, int grid, cudaStream_t st) {
+  size_t sm = Smem<B>::bytes(p.T, p.k);
+  cudaError_t e = cudaFuncSetAttribute(k_accumulate_topk<B, KS, SINT8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  k_accumulate_topk<B, KS, SINT8><<<grid, kThreads, sm, st>>>(p);
+  return cudaGetLastError();
+}
+
 template <int B, int KS>
 cudaError_t launch_main(const QP& p, int grid, cudaStream_t st) {
-  size_t sm = Smem<B>::bytes(p.T, p.k);
-  cudaError_t e = cudaFuncSetAttribute(k_accumulate_topk<B, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (e != cudaSuccess) return e;
-  k_accumulate_topk<B, KS><<<grid, kThreads, sm, st>>>(p);
-  return cudaGetLastError();
+  return p.vals ? launch_main3<B, KS, true>(p, grid, st) : launch_main3<B, KS, false>(p, grid, st);
 }
 
 template <int B>

@@ -180,7 +180,7 @@ def test_index_layout_matches_scipy_csc():
             a, b = off[f * (NT + 1) + t], off[f * (NT + 1) + t + 1]
             got_ids = ids[8 * a:8 * b]
             got_vals = vals[8 * a:8 * b]
-            keep = got_ids != 0xFFFF
+            keep = got_ids < T
             order = np.argsort(got_ids[keep])
             sel = (rows_f >= t * T) & (rows_f < (t + 1) * T)
             np.testing.assert_array_equal(got_ids[keep][order].astype(np.int64), rows_f[sel] - t * T)
