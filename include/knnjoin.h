@@ -60,27 +60,39 @@ typedef struct {
 } knnjoin_csr;
 
 /* Build options.  tile: S ids per tile (the S-block of Alg. 1 mapped to a shared-memory score array);
- * 0 = default 8192; must be a multiple of 2048 and <= 32768 (local ids are 15-bit).
- * prune / alpha: reserved for the threshold-pruned mode; must be 0 / 0. */
+ * 0 = default 8192; must be a multiple of 2048 and <= 32768.
+ * prune / alpha: reserved for the threshold-pruned mode; must be 0 / 0.
+ * dense_min: encoding of dense slices (BINARY S only).  A slice (I_f restricted to one tile) with at least
+ *   dense_min postings is stored as a tile-wide bitmap (tile/8 bytes) instead of a list of local ids, and
+ *   its scores are accumulated in registers during the top-k scan instead of by shared-memory atomics.
+ *   0 = default (tile/4 postings, i.e. density >= 1/4); -1 = never (every slice is an id list).  Values
+ *   below tile/16 are raised to tile/16 (a bitmap is then never larger than the id list it replaces). */
 typedef struct {
   int32_t tile;
   int32_t prune;
   float alpha;
+  int32_t dense_min;
 } knnjoin_options;
 
 /* Query options (all optional; pass NULL for defaults).
- *  batch_rows: R rows per CTA batch (0 = auto: the largest of {8,6,4,2,1} whose score arrays fit in
- *              shared memory for this tile width and k).
+ *  batch_rows: R rows per CTA batch (0 = auto).
+ *  cta_warps:  warps per CTA of the accumulation kernel, 8 or 16 (0 = auto: 8-warp CTAs, two per SM,
+ *              with the largest batch whose score arrays fit; else one 16-warp CTA per SM).
  *  counters:   NULL, or a device int64_t[4] that the query ADDS into: [0] postings visited (Eq. 4 second
  *              term), [1] candidate inserts into the top-k lists, [2] postings skipped by
  *              pruning (0 in unpruned mode), [3] completions (0 in unpruned mode).
  *  ev_begin / ev_end: NULL, or cudaEvent_t (as void*) recorded on `stream` immediately before and after
- *              the score-accumulation + top-k kernel, so callers can time that kernel alone. */
+ *              the score-accumulation + top-k kernel, so callers can time that kernel alone.
+ *  phase_cycles: NULL, or a device int64_t[8] that the query ADDS SM clock cycles into, summed over CTAs
+ *              (thread 0 of each CTA): [0] staging, [1] sparse atomics, [2] dense pass, [3] scan + top-k,
+ *              [4] list merge + output, [5] batch fetch / setup.  Profiling aid; off when NULL. */
 typedef struct {
   int32_t batch_rows;
   int64_t* counters;
   void* ev_begin;
   void* ev_end;
+  int64_t* phase_cycles;
+  int32_t cta_warps;
 } knnjoin_query_options;
 
 typedef struct knnjoin_index knnjoin_index; /* opaque HOST handle; borrows the caller's index storage */
@@ -95,6 +107,7 @@ typedef struct {
   int64_t unit_capacity;/* 16-byte posting units reserved in the storage (upper bound) */
   int64_t storage_bytes;/* bytes of index storage the handle uses */
   knnjoin_dtype s_dtype;
+  int32_t dense_min;    /* postings per slice from which a slice is a bitmap (INT32_MAX = never) */
 } knnjoin_index_info;
 
 /* ---- index build: Create_Inverted_List_IIB (Alg. 3 lines 5-8) on the device ------ */
@@ -109,8 +122,9 @@ size_t knnjoin_build_workspace_bytes(const knnjoin_csr* S, int32_t d, const knnj
 /* Build the tiled inverted index of S into `index_storage` (>= knnjoin_index_bytes bytes, 256-byte
  * aligned) using `workspace` (>= knnjoin_build_workspace_bytes bytes).  Layout:
  * for tile t (S ids [t*tile, (t+1)*tile)) and feature f, the postings of I_f restricted to the tile are a
- * contiguous, 16-byte aligned slice of 15-bit local ids (+ uint8 values for INT8 S), padded with the
- * sentinel 0xFFFF, permuted inside each 256-posting block so a warp's 32 lanes touch consecutive ids.
+ * contiguous, 16-byte aligned slice of local ids (+ uint8 values for INT8 S), padded with dummy ids
+ * tile + (0..31), permuted inside each 256-posting block so a warp's 32 lanes touch consecutive ids;
+ * dense slices (see dense_min) are tile-wide bitmaps, flagged by bit 31 of their start offset.
  * s_id_base: global id of S row 0 (ids returned by queries are s_id_base + local row).
  * S may be freed after the call's work completes on `stream`; the storage must outlive every query.
  * S dtype must be BINARY or INT8 (FP32 S -> KNNJOIN_ERR_UNSUPPORTED).  *out receives a host handle

@@ -31,18 +31,20 @@ class _CSR(ctypes.Structure):
 
 
 class _Options(ctypes.Structure):
-    _fields_ = [("tile", ctypes.c_int32), ("prune", ctypes.c_int32), ("alpha", ctypes.c_float)]
+    _fields_ = [("tile", ctypes.c_int32), ("prune", ctypes.c_int32), ("alpha", ctypes.c_float),
+                ("dense_min", ctypes.c_int32)]
 
 
 class _QueryOptions(ctypes.Structure):
     _fields_ = [("batch_rows", ctypes.c_int32), ("counters", ctypes.c_void_p), ("ev_begin", ctypes.c_void_p),
-                ("ev_end", ctypes.c_void_p)]
+                ("ev_end", ctypes.c_void_p), ("phase_cycles", ctypes.c_void_p), ("cta_warps", ctypes.c_int32)]
 
 
 class _IndexInfo(ctypes.Structure):
     _fields_ = [("n_s", ctypes.c_int64), ("s_id_base", ctypes.c_int64), ("d", ctypes.c_int32),
                 ("tile", ctypes.c_int32), ("n_tiles", ctypes.c_int64), ("offsets", ctypes.c_int64),
-                ("unit_capacity", ctypes.c_int64), ("storage_bytes", ctypes.c_int64), ("s_dtype", ctypes.c_int)]
+                ("unit_capacity", ctypes.c_int64), ("storage_bytes", ctypes.c_int64), ("s_dtype", ctypes.c_int),
+                ("dense_min", ctypes.c_int32)]
 
 
 def library_path() -> str:
@@ -180,9 +182,9 @@ def _empty_u8(nbytes: int, device) -> torch.Tensor:
 
 
 def knnjoin_build_index(S: DeviceCSR, d: int, s_id_base: int = 0, tile: int = 0, stream=None,
-                        workspace: torch.Tensor | None = None) -> Index:
+                        workspace: torch.Tensor | None = None, dense_min: int = 0) -> Index:
     cS = S._c()
-    opt = _Options(tile, 0, 0.0)
+    opt = _Options(tile, 0, 0.0, dense_min)
     nbytes = _lib.knnjoin_index_bytes(ctypes.byref(cS), d, ctypes.byref(opt))
     if nbytes == 0:
         raise KnnJoinError(1, "knnjoin_index_bytes", knnjoin_last_error())
@@ -209,13 +211,15 @@ def knnjoin_index_stats(index: Index) -> dict:
 
 def knnjoin_query(index: Index, R: DeviceCSR, k: int, want_keys: bool = False, want_ids: bool = True,
                   batch_rows: int = 0, counters: torch.Tensor | None = None, events=None, stream=None,
-                  workspace: torch.Tensor | None = None):
+                  workspace: torch.Tensor | None = None, phase_cycles: torch.Tensor | None = None,
+                  cta_warps: int = 0):
     """Returns (ids int32 [n,k], scores float32 [n,k], keys uint64-as-int64 [n,k] or None)."""
     cR = R._c()
     if events and (events[0].cuda_event == 0 or events[1].cuda_event == 0):
         raise ValueError("timing events must have been recorded once (so their cudaEvent handles exist)")
     qo = _QueryOptions(batch_rows, counters.data_ptr() if counters is not None else 0,
-                       events[0].cuda_event if events else 0, events[1].cuda_event if events else 0)
+                       events[0].cuda_event if events else 0, events[1].cuda_event if events else 0,
+                       phase_cycles.data_ptr() if phase_cycles is not None else 0, cta_warps)
     wbytes = _lib.knnjoin_query_workspace_bytes(index.handle, ctypes.byref(cR), k, ctypes.byref(qo))
     if wbytes == 0:
         raise KnnJoinError(1, "knnjoin_query_workspace_bytes", knnjoin_last_error())

@@ -20,6 +20,8 @@ constexpr int kMaxK = 256;
 constexpr int kDefaultTile = 8192;
 constexpr int kMaxTile = 32768;        // local ids < tile; padding ids are tile + (0..31) (dummy columns)
 constexpr int kTileQuantum = 2048;     // tile must split into kWarps column strips of 128-column chunks
+constexpr uint32_t kDenseFlag = 0x80000000u;
+constexpr uint32_t kOffMask = 0x7FFFFFFFu;
 constexpr int kPadCols = 32;           // dummy score columns per row that absorb padding postings
 constexpr uint64_t kKeyFloor = 0x00000000FFFFFFFFull;  // score 0 with every id: admits nothing
 constexpr double kFixedOne = 1073741824.0;              // 2^30: per-row fixed-point scale numerator
@@ -52,7 +54,9 @@ struct knnjoin_index {
   int32_t d = 0, tile = 0;
   int64_t n_tiles = 0, n_off = 0, unit_cap = 0;
   knnjoin_dtype s_dtype = KNNJOIN_BINARY;
-  const uint32_t* off = nullptr;  // [n_off] posting-unit (16 B) offsets, feature-major: f*(n_tiles+1)+t
+  int32_t dense_min = 0x7FFFFFFF;  // slices with >= dense_min postings are tile-wide bitmaps
+  const uint32_t* off = nullptr;  // [n_off] posting-unit (16 B) offsets, feature-major: f*(n_tiles+1)+t;
+                                  // bit 31 set: the slice starting here is a bitmap (tile/128 units)
   const int32_t* df = nullptr;    // [d] |I_d| (document frequency of each feature in S)
   const uint16_t* ids = nullptr;  // [unit_cap*8] local S ids (< tile); padding = tile + (u mod 32)
   const uint8_t* vals = nullptr;  // [unit_cap*8] INT8 S weights (nullptr for BINARY S)

@@ -10,16 +10,20 @@
 //                                                            entries hold tile + (u mod 32), a dummy column
 //   vals[8*u .. 8*u+8)                                       INT8 S weights (same positions)
 //
-// Steps (all stream-ordered, integer, deterministic):
-//   1. k_count     key(s, f) = f*(n_tiles+1) + t(s); histogram of keys; df[f] (= |I_f|)
-//   2. k_units     units(key) = ceil(count/8)   (16-byte alignment of every slice)
-//   3. CUB exclusive scans: off = scan(units), first = scan(count)
-//   4. CUB stable radix sort of (key, s) pairs -- CSR order is ascending s, so each key's postings come
+// Steps (all stream-ordered, integer, deterministic, no contended atomics -- Zipf head features put every
+// row of a tile on the same key, so a global-atomic histogram would serialise):
+//   1. k_keys      key(s, f) = f*(n_tiles+1) + t(s) for every nonzero, value = (local id, weight)
+//   2. CUB stable radix sort of (key, value) pairs -- CSR order is ascending s, so each key's postings come
 //      out in ascending s (Alg. 3 inserts "in B_s scan order")
+//   3. k_seg_first / k_seg_count: run-length of equal keys -> first[key], counts[key]; k_df: df[f] = |I_f|
+//   4. k_units     units(key) = ceil(count/8) (16-byte alignment), or tile/128 for a bitmap slice;
+//      CUB exclusive scan: off = scan(units)
 //   5. k_scatter   posting of sorted rank rho inside slice goes to block rho/256, and inside a block of m
 //      units to lane i = rho%m, slot j = rho/m (unit i holds sorted postings i, i+m, ..., i+7m): when a
 //      warp's lane i loads unit i and issues atomic j, the 32 lanes hit 32 consecutive ids of a dense
 //      slice -> 32 distinct shared-memory banks.
+//      Dense slices (>= dense_min postings, BINARY S) are instead a tile-wide bitmap (bit = local id).
+//   6. k_mark_dense sets bit 31 of a dense slice's start offset.
 // The paper counts this as Eq. 4's first term, sum |s_i| postings.
 #include <cub/cub.cuh>
 
@@ -51,6 +55,16 @@ bool index_layout(const knnjoin_csr* S, int32_t d, int32_t tile, IndexLayout* L)
   if (S->dtype == KNNJOIN_INT8) at = align_up(at + 8 * (size_t)L->unit_cap, 256);
   L->total = at;
   return true;
+}
+
+// postings from which a slice is stored as a bitmap (0xFFFFFFFF = never); BINARY S only
+uint32_t dense_threshold(const knnjoin_csr* S, int32_t tile, const knnjoin_options* opt) {
+  if (S->dtype != KNNJOIN_BINARY) return 0xFFFFFFFFu;
+  int32_t v = opt ? opt->dense_min : 0;
+  if (v < 0) return 0xFFFFFFFFu;
+  if (v == 0) v = tile / 4;
+  if (v < tile / 16) v = tile / 16;
+  return (uint32_t)v;
 }
 
 namespace {
@@ -110,10 +124,9 @@ bool check_build_args(const knnjoin_csr* S, int32_t d, const knnjoin_options* op
 }
 
 // warp per S row
-__global__ void k_count(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                        const int8_t* __restrict__ values, int64_t n_s, int32_t d, int32_t tile, int64_t n_tiles,
-                        uint32_t* __restrict__ counts, int32_t* __restrict__ df, uint32_t* __restrict__ keys,
-                        uint32_t* __restrict__ vals, uint32_t sentinel_key) {
+__global__ void k_keys(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                       const int8_t* __restrict__ values, int64_t n_s, int32_t d, int32_t tile, int64_t n_tiles,
+                       uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, uint32_t sentinel_key) {
   int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (row >= n_s) return;
@@ -122,17 +135,43 @@ __global__ void k_count(const int64_t* __restrict__ indptr, const int32_t* __res
   for (int64_t j = indptr[row] + lane; j < indptr[row + 1]; j += 32) {
     int32_t f = indices[j];
     if (f >= 0 && f < d) {
-      uint32_t key = (uint32_t)((int64_t)f * (n_tiles + 1) + t);
-      atomicAdd(&counts[key], 1u);
-      atomicAdd(&df[f], 1);
-      uint32_t v = values ? (uint32_t)(uint8_t)values[j] : 0u;
-      keys[j] = key;
-      vals[j] = local | (v << 16);
+      keys[j] = (uint32_t)((int64_t)f * (n_tiles + 1) + t);
+      vals[j] = local | ((values ? (uint32_t)(uint8_t)values[j] : 0u) << 16);
     } else {
       keys[j] = sentinel_key;
       vals[j] = 0;
     }
   }
+}
+
+// first sorted position of every present key
+__global__ void k_seg_first(const uint32_t* __restrict__ keys, int64_t nnz, uint32_t sentinel_key,
+                            uint32_t* __restrict__ first) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nnz) return;
+  uint32_t k = keys[i];
+  if (k < sentinel_key && (i == 0 || keys[i - 1] != k)) first[k] = (uint32_t)i;
+}
+
+// posting count of every present key (absent keys keep the memset 0)
+__global__ void k_seg_count(const uint32_t* __restrict__ keys, int64_t nnz, uint32_t sentinel_key,
+                            const uint32_t* __restrict__ first, uint32_t* __restrict__ counts) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nnz) return;
+  uint32_t k = keys[i];
+  if (k < sentinel_key && (i == nnz - 1 || keys[i + 1] != k)) counts[k] = (uint32_t)(i + 1) - first[k];
+}
+
+// warp per feature: df[f] = sum over tiles of counts[f][t]
+__global__ void k_df(const uint32_t* __restrict__ counts, int32_t d, int64_t n_tiles, int32_t* __restrict__ df) {
+  int64_t f = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (f >= d) return;
+  uint32_t s = 0;
+  for (int64_t t = lane; t < n_tiles; t += 32) s += counts[f * (n_tiles + 1) + t];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) df[f] = (int32_t)s;
 }
 
 // padding entries point at one of 32 dummy score columns [tile, tile+32) (spread over banks by unit index),
@@ -145,20 +184,45 @@ __global__ void k_fill_pads(uint4* __restrict__ ids, int64_t units, uint32_t til
   ids[u] = make_uint4(pad, pad, pad, pad);
 }
 
-__global__ void k_units(const uint32_t* __restrict__ counts, uint32_t* __restrict__ units, int64_t n) {
+__global__ void k_units(const uint32_t* __restrict__ counts, uint32_t* __restrict__ units, int64_t n,
+                        uint32_t dense_min, uint32_t dense_units) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) units[i] = (counts[i] + 7u) >> 3;
+  if (i < n) {
+    uint32_t c = counts[i];
+    units[i] = c >= dense_min ? dense_units : (c + 7u) >> 3;
+  }
+}
+
+// zero the bitmap of every dense slice (the pad fill wrote dummy ids there)
+__global__ void k_zero_dense(const uint32_t* __restrict__ counts, const uint32_t* __restrict__ off, int64_t n,
+                             uint32_t dense_min, uint32_t dense_units, uint4* __restrict__ ids) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || counts[i] < dense_min) return;
+  uint4* b = ids + off[i];
+  for (uint32_t u = 0; u < dense_units; ++u) b[u] = make_uint4(0, 0, 0, 0);
+}
+
+__global__ void k_mark_dense(const uint32_t* __restrict__ counts, uint32_t* __restrict__ off, int64_t n,
+                             uint32_t dense_min) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && counts[i] >= dense_min) off[i] |= kDenseFlag;
 }
 
 __global__ void k_scatter(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, int64_t nnz,
                           const uint32_t* __restrict__ off, const uint32_t* __restrict__ first,
-                          uint32_t sentinel_key, uint16_t* __restrict__ ids, uint8_t* __restrict__ wvals) {
+                          const uint32_t* __restrict__ counts, uint32_t dense_min, uint32_t sentinel_key,
+                          uint16_t* __restrict__ ids, uint8_t* __restrict__ wvals) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nnz) return;
   uint32_t key = keys[i];
   if (key >= sentinel_key) return;
-  uint32_t rank = (uint32_t)i - first[key];
   uint32_t u0 = off[key];
+  if (counts[key] >= dense_min) {  // bitmap slice: bit `local id`
+    uint32_t local = vals[i] & 0xFFFFu;
+    atomicOr((uint32_t*)ids + (size_t)u0 * 4 + (local >> 5), 1u << (local & 31));
+    return;
+  }
+  uint32_t rank = (uint32_t)i - first[key];
   uint32_t U = off[key + 1] - u0;
   uint32_t beta = rank >> 8, iota = rank & 255u;
   uint32_t m = U - 32u * beta;
@@ -230,32 +294,46 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   uint32_t* vb = (uint32_t*)(wb + W.vb_at);
   void* cubtmp = wb + W.cub_at;
   uint32_t sentinel_key = (uint32_t)(L.n_off - 1);
+  const uint32_t dense_min = dense_threshold(S, tile, opt);
+  const uint32_t dense_units = (uint32_t)tile / 128u;
 
   cudaError_t e;
   if ((e = cudaMemsetAsync(counts, 0, 4 * (size_t)L.n_off, st)) != cudaSuccess) return cuda_fail(e, "memset counts");
-  if ((e = cudaMemsetAsync(df, 0, 4 * (size_t)d, st)) != cudaSuccess) return cuda_fail(e, "memset df");
-  k_fill_pads<<<(unsigned)((L.unit_cap + 255) / 256), 256, 0, st>>>((uint4*)ids, L.unit_cap, (uint32_t)tile);
-  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_fill_pads");
   if (vals && (e = cudaMemsetAsync(vals, 0, 8 * (size_t)L.unit_cap, st)) != cudaSuccess) return cuda_fail(e, "memset vals");
-  if (S->n_rows > 0) {
-    int64_t threads = S->n_rows * 32;
-    k_count<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(S->indptr, S->indices, (const int8_t*)S->values,
-                                                             S->n_rows, d, tile, L.n_tiles, counts, df, ka, va,
-                                                             sentinel_key);
-    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_count");
-  }
-  k_units<<<(unsigned)((L.n_off + 255) / 256), 256, 0, st>>>(counts, units, L.n_off);
-  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_units");
-  size_t tb = W.cub_bytes;
-  if ((e = cub::DeviceScan::ExclusiveSum(cubtmp, tb, units, off, (int)L.n_off, st)) != cudaSuccess) return cuda_fail(e, "scan off");
-  tb = W.cub_bytes;
-  if ((e = cub::DeviceScan::ExclusiveSum(cubtmp, tb, counts, first, (int)L.n_off, st)) != cudaSuccess) return cuda_fail(e, "scan first");
+  const unsigned gnnz = (unsigned)((S->nnz + 255) / 256);
   if (S->nnz > 0) {
-    tb = W.cub_bytes;
+    int64_t threads = S->n_rows * 32;
+    k_keys<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(S->indptr, S->indices, (const int8_t*)S->values,
+                                                            S->n_rows, d, tile, L.n_tiles, ka, va, sentinel_key);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_keys");
+    size_t tb = W.cub_bytes;
     if ((e = cub::DeviceRadixSort::SortPairs(cubtmp, tb, ka, kb, va, vb, (int)S->nnz, 0, end_bit_for(L.n_off - 1), st)) != cudaSuccess)
       return cuda_fail(e, "radix sort");
-    k_scatter<<<(unsigned)((S->nnz + 255) / 256), 256, 0, st>>>(kb, vb, S->nnz, off, first, sentinel_key, ids, vals);
+    k_seg_first<<<gnnz, 256, 0, st>>>(kb, S->nnz, sentinel_key, first);
+    k_seg_count<<<gnnz, 256, 0, st>>>(kb, S->nnz, sentinel_key, first, counts);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_seg");
+  }
+  k_df<<<(unsigned)(((int64_t)d * 32 + 255) / 256), 256, 0, st>>>(counts, d, L.n_tiles, df);
+  k_units<<<(unsigned)((L.n_off + 255) / 256), 256, 0, st>>>(counts, units, L.n_off, dense_min, dense_units);
+  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_units");
+  {
+    size_t tb = W.cub_bytes;
+    if ((e = cub::DeviceScan::ExclusiveSum(cubtmp, tb, units, off, (int)L.n_off, st)) != cudaSuccess) return cuda_fail(e, "scan off");
+  }
+  k_fill_pads<<<(unsigned)((L.unit_cap + 255) / 256), 256, 0, st>>>((uint4*)ids, L.unit_cap, (uint32_t)tile);
+  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_fill_pads");
+  if (S->nnz > 0) {
+    if (dense_min != 0xFFFFFFFFu) {
+      k_zero_dense<<<(unsigned)((L.n_off - 1 + 255) / 256), 256, 0, st>>>(counts, off, L.n_off - 1, dense_min,
+                                                                        dense_units, (uint4*)ids);
+      if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_zero_dense");
+    }
+    k_scatter<<<gnnz, 256, 0, st>>>(kb, vb, S->nnz, off, first, counts, dense_min, sentinel_key, ids, vals);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_scatter");
+    if (dense_min != 0xFFFFFFFFu) {
+      k_mark_dense<<<(unsigned)((L.n_off - 1 + 255) / 256), 256, 0, st>>>(counts, off, L.n_off - 1, dense_min);
+      if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_mark_dense");
+    }
   }
   knnjoin_index* h = new (std::nothrow) knnjoin_index();
   if (!h) { set_error("host allocation failed"); return KNNJOIN_ERR_ARG; }
@@ -267,6 +345,7 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   h->n_off = L.n_off;
   h->unit_cap = L.unit_cap;
   h->s_dtype = S->dtype;
+  h->dense_min = dense_min == 0xFFFFFFFFu ? 0x7FFFFFFF : (int32_t)dense_min;
   h->off = off;
   h->df = df;
   h->ids = ids;
@@ -287,6 +366,7 @@ KJ_API knnjoin_status knnjoin_index_stats(const knnjoin_index* idx, knnjoin_inde
   out->unit_capacity = idx->unit_cap;
   out->storage_bytes = (int64_t)idx->storage_bytes;
   out->s_dtype = idx->s_dtype;
+  out->dense_min = idx->dense_min;
   return KNNJOIN_OK;
 }
 

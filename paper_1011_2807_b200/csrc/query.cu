@@ -48,6 +48,7 @@ struct QP {
   const double* inv_sigma;
   uint32_t* batch_counter;
   unsigned long long* counters;
+  unsigned long long* phase;  // [8] cycles per phase (profiling), or nullptr
   // out
   uint64_t* out_keys;
   int32_t* out_ids;
@@ -144,6 +145,7 @@ __global__ void k_build_runs(const int64_t* __restrict__ indptr, const int32_t* 
 }
 
 // -------------------------------------------------------------------------- block-wide scan helper
+template <int NW>
 __device__ __forceinline__ uint64_t block_exclusive_scan_u64(uint64_t v, uint64_t* s_warp, uint64_t* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint64_t x = v;
@@ -155,17 +157,17 @@ __device__ __forceinline__ uint64_t block_exclusive_scan_u64(uint64_t v, uint64_
   if (lane == 31) s_warp[warp] = x;
   __syncthreads();
   if (warp == 0) {
-    uint64_t w = lane < kWarps ? s_warp[lane] : 0;
+    uint64_t w = lane < NW ? s_warp[lane] : 0;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
       if (lane >= o) w += y;
     }
-    if (lane < kWarps) s_warp[lane] = w;  // inclusive warp totals
+    if (lane < NW) s_warp[lane] = w;  // inclusive warp totals
   }
   __syncthreads();
   uint64_t before = warp ? s_warp[warp - 1] : 0;
-  *total = s_warp[kWarps - 1];
+  *total = s_warp[NW - 1];
   return before + x - v;
 }
 
@@ -173,57 +175,110 @@ __device__ __forceinline__ uint64_t block_exclusive_scan_u64(uint64_t v, uint64_
 // Score rows have stride T + kPadCols: columns [T, T+32) absorb padding postings (never scanned).
 __host__ __device__ inline int acc_stride(int T) { return T + kPadCols; }
 
-// the score array doubles as the scratch of the end-of-batch list merge ([kWarps][B][k] keys)
-__host__ __device__ inline size_t acc_region_bytes(int B, int T, int k) {
-  size_t a = (size_t)B * acc_stride(T) * 4, m = (size_t)kWarps * B * k * 8;
+// the score array doubles as the scratch of the end-of-batch list merge ([NW][B][k] keys)
+__host__ __device__ inline size_t acc_region_bytes(int B, int T, int k, int NW) {
+  size_t a = (size_t)B * acc_stride(T) * 4, m = (size_t)NW * B * k * 8;
   return align_up(a > m ? a : m, 16);
 }
 
-template <int B>
-struct Smem {
-  static size_t bytes(int T, int k) {
-    size_t at = acc_region_bytes(B, T, k);          // acc / merge scratch
-    at += (size_t)kCap * 4;                        // ustart
-    at += (size_t)(kCap + 1) * 4;                  // P
-    at += (size_t)kCap * 4;                        // fm
-    at += (size_t)kCap * B * 4;                    // q
-    at = align_up(at, 16);
-    at += kWarps * 8;                              // scan partials
-    at += 8 * 8;                                   // theta_row (B <= 8)
-    at += 16;                                      // misc
-    return at;
-  }
-};
+// shared-memory layout of k_accumulate_topk<B, ., ., NW>; the kernel derives its pointers from the same sums
+__host__ __device__ inline size_t staging_at(int B, int T, int k, int NW) { return acc_region_bytes(B, T, k, NW); }
+__host__ __device__ inline size_t tail_at(int B, int T, int k, int NW) {
+  return align_up(staging_at(B, T, k, NW) + (size_t)kCap * 4 + (size_t)(kCap + 1) * 4 + (size_t)kCap * 4 +
+                      (size_t)kCap * B * 4, 16);
+}
+__host__ __device__ inline size_t smem_bytes(int B, int T, int k, int NW) {
+  return tail_at(B, T, k, NW) + (size_t)NW * 8 /* scan partials */ + 8 * 8 /* theta_row */ + 32 /* misc */;
+}
 
 __device__ __forceinline__ void red_add_shared(uint32_t addr, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
+// Adds the dense (bitmap) slices staged at [kCap - n_dense, kCap) to the 4 columns [seg0 + 4*lane, +4) of
+// every batch row: v[b][j] += q_b if bit(col) is set (q_b is 0 for rows without the feature, so no per-run
+// row mask is consulted).  seg0 is the first column of the warp's 128-column step.  Returns the number of
+// (posting, row) visits applied by this lane when counting is on.
+__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+template <int B, bool COUNT>
+__device__ __forceinline__ unsigned long long dense_add(uint32_t (&v)[B][4], int seg0, int n_dense,
+                                                        const uint16_t* __restrict__ ids, const uint32_t* s_ustart,
+                                                        const uint32_t* s_fm, const int32_t* s_q, int lane) {
+  const uint32_t* words = (const uint32_t*)ids + (seg0 >> 5) + (lane >> 3);
+  const int sh = (lane & 7) * 4;
+  unsigned long long nv = 0;
+  constexpr int U = 4;
+  uint32_t w[U];
+  int e0 = kCap - n_dense;
+#pragma unroll
+  for (int u = 0; u < U; ++u) w[u] = (e0 + u < kCap) ? __ldg(words + (size_t)s_ustart[e0 + u] * 4) : 0u;
+  for (; e0 < kCap; e0 += U) {
+    uint32_t wn[U];  // next group's bitmap words, in flight while this group is applied
+#pragma unroll
+    for (int u = 0; u < U; ++u) wn[u] = (e0 + U + u < kCap) ? __ldg(words + (size_t)s_ustart[e0 + U + u] * 4) : 0u;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (e0 + u < kCap) {
+        const uint32_t nib = w[u] >> sh;
+        const uint32_t b0 = nib & 1u, b1 = (nib >> 1) & 1u, b2 = (nib >> 2) & 1u, b3 = (nib >> 3) & 1u;
+        const int32_t* q = s_q + (e0 + u) * B;
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+          const uint32_t qb = (uint32_t)q[b];
+          v[b][0] = mad_u32(b0, qb, v[b][0]);
+          v[b][1] = mad_u32(b1, qb, v[b][1]);
+          v[b][2] = mad_u32(b2, qb, v[b][2]);
+          v[b][3] = mad_u32(b3, qb, v[b][3]);
+        }
+        if (COUNT) nv += (unsigned long long)__popc(nib & 0xFu) * __popc(s_fm[e0 + u] >> 24);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) w[u] = wn[u];
+  }
+  return nv;
+}
+
 constexpr int kWinChunk = 4;  // 32-unit windows a warp takes per grab of the dynamic window counter
 
-template <int B, int KS, bool SINT8>
-__global__ void __launch_bounds__(kThreads, 1) k_accumulate_topk(QP p) {
+template <int B, int KS, bool SINT8, int NW>
+__global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
+  constexpr int NT_ = NW * 32;        // threads per CTA
+  constexpr int IPT = kCap / NT_;     // staged runs per thread
   extern __shared__ __align__(16) unsigned char smem[];
   const int T = p.T;
   const int TS = acc_stride(T);
   uint32_t* acc = (uint32_t*)smem;
   const uint32_t acc_s = (uint32_t)__cvta_generic_to_shared(acc);
-  uint32_t* s_ustart = (uint32_t*)(smem + acc_region_bytes(B, T, p.k));
+  uint32_t* s_ustart = (uint32_t*)(smem + staging_at(B, T, p.k, NW));
   uint32_t* s_P = s_ustart + kCap;
   uint32_t* s_fm = s_P + kCap + 1;
   int32_t* s_q = (int32_t*)(s_fm + kCap);
-  size_t at = align_up(acc_region_bytes(B, T, p.k) + (size_t)kCap * 4 + (size_t)(kCap + 1) * 4 + (size_t)kCap * 4 +
-                           (size_t)kCap * B * 4, 16);
-  uint64_t* s_warp = (uint64_t*)(smem + at);
-  uint64_t* s_theta = s_warp + kWarps;
-  int* s_misc = (int*)(s_theta + 8);  // [0] batch, [1] n_items, [2] TOT, [3] window counter
+  uint64_t* s_warp = (uint64_t*)(smem + tail_at(B, T, p.k, NW));
+  uint64_t* s_theta = s_warp + NW;
+  int* s_misc = (int*)(s_theta + 8);  // [0] batch, [1] n sparse items, [2] TOT, [3] window counter, [4] n dense
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = p.k;
   constexpr bool wint8 = SINT8;
+  const bool timing = p.phase != nullptr && tid == 0;
+  unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};
+  long long t_mark = timing ? clock64() : 0;
+  auto phase_mark = [&](int i) {
+    if (timing) {
+      const long long now = clock64();
+      ph[i] += (unsigned long long)(now - t_mark);
+      t_mark = now;
+    }
+  };
   unsigned long long n_visits = 0, n_inserts = 0;
 
-  for (int i = tid; i < (int)(acc_region_bytes(B, T, k) / 16); i += kThreads) ((uint4*)acc)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = tid; i < (int)(acc_region_bytes(B, T, k, NW) / 16); i += NT_) ((uint4*)acc)[i] = make_uint4(0, 0, 0, 0);
 
   for (;;) {
     __syncthreads();
@@ -246,39 +301,60 @@ __global__ void __launch_bounds__(kThreads, 1) k_accumulate_topk(QP p) {
       for (int s = 0; s < KS; ++s) L[b][s] = 0;
     }
     __syncthreads();
+    phase_mark(5);
 
     const int64_t ntiles = nruns > 0 ? p.NT : 0;
     for (int64_t t = 0; t < ntiles; ++t) {
       for (int c0 = 0; c0 < nruns; c0 += kCap) {
         // ---------------------------------------------------------------- stage chunk of runs
+        // sparse (id-list) slices are compacted to the front with their position P in the flattened unit
+        // stream; dense (bitmap) slices are compacted to the back, [kCap - n_dense, kCap)
         {
-          const int i = c0 + tid;
-          uint32_t fm = 0, u0 = 0, U = 0;
-          size_t run = (size_t)(run_base + i);
-          if (i < nruns) {
-            fm = p.runs_f[run];
-            const uint32_t* o = p.off + (size_t)(fm & 0xFFFFFFu) * (size_t)(p.NT + 1) + (size_t)t;
-            u0 = o[0];
-            U = o[1] - u0;
-          }
-          const uint64_t packed = ((uint64_t)(U > 0) << 32) | U;
-          uint64_t total;
-          const uint64_t ex = block_exclusive_scan_u64(packed, s_warp, &total);
-          if (U > 0) {
-            const uint32_t c = (uint32_t)(ex >> 32);
-            s_ustart[c] = u0;
-            s_P[c] = (uint32_t)ex;
-            s_fm[c] = fm;
+          uint32_t fm[IPT], u0[IPT], U[IPT];
+          uint64_t pk[IPT], mine = 0;
 #pragma unroll
-            for (int b = 0; b < B; ++b) s_q[c * B + b] = p.runs_q[run * B + b];
+          for (int it = 0; it < IPT; ++it) {
+            const int i = c0 + tid * IPT + it;
+            fm[it] = 0; u0[it] = 0; U[it] = 0;
+            bool dense = false;
+            if (i < nruns) {
+              fm[it] = p.runs_f[(size_t)(run_base + i)];
+              const uint32_t* o = p.off + (size_t)(fm[it] & 0xFFFFFFu) * (size_t)(p.NT + 1) + (size_t)t;
+              const uint32_t a0 = o[0], a1 = o[1];
+              dense = (a0 & kDenseFlag) != 0;
+              u0[it] = a0 & kOffMask;
+              U[it] = (a1 & kOffMask) - u0[it];
+            }
+            const bool sp = !dense && U[it] > 0;
+            pk[it] = ((uint64_t)dense << 48) | ((uint64_t)sp << 32) | (sp ? U[it] : 0u);
+            mine += pk[it];
+          }
+          uint64_t total;
+          uint64_t ex = block_exclusive_scan_u64<NW>(mine, s_warp, &total);
+#pragma unroll
+          for (int it = 0; it < IPT; ++it) {
+            const bool dense = (pk[it] >> 48) != 0, sp = ((pk[it] >> 32) & 0xFFFFu) != 0;
+            if (sp || dense) {
+              const uint32_t c = sp ? (uint32_t)((ex >> 32) & 0xFFFFu) : (uint32_t)(kCap - 1 - (int)(ex >> 48));
+              s_ustart[c] = u0[it];
+              if (sp) s_P[c] = (uint32_t)ex;
+              s_fm[c] = fm[it];
+              const size_t run = (size_t)(run_base + c0 + tid * IPT + it);
+#pragma unroll
+              for (int b = 0; b < B; ++b) s_q[c * B + b] = p.runs_q[run * B + b];
+            }
+            ex += pk[it];
           }
           if (tid == 0) {
-            s_misc[1] = (int)(total >> 32);
+            const uint32_t ns = (uint32_t)((total >> 32) & 0xFFFFu);
+            s_misc[1] = (int)ns;
             s_misc[2] = (int)(uint32_t)total;
             s_misc[3] = 0;
-            s_P[(uint32_t)(total >> 32)] = (uint32_t)total;
+            s_misc[4] = (int)(total >> 48);
+            s_P[ns] = (uint32_t)total;
           }
           __syncthreads();
+          phase_mark(0);
         }
         // ---------------------------------------------------------------- accumulate (a4)
         {
@@ -375,42 +451,80 @@ __global__ void __launch_bounds__(kThreads, 1) k_accumulate_topk(QP p) {
             }
           }
           __syncthreads();
+          phase_mark(1);
+        }
+        // ---------------------------------------------------------------- dense slices of a non-final chunk
+        if (c0 + kCap < nruns && s_misc[4] > 0) {
+          const int n_dense = s_misc[4];
+          const int cols = T / NW;
+          for (int c = 0; c < cols; c += 128) {
+            const int col = warp * cols + c + lane * 4;
+            uint32_t v[B][4];
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+              const uint4 x = *(const uint4*)(acc + (size_t)b * TS + col);
+              v[b][0] = x.x; v[b][1] = x.y; v[b][2] = x.z; v[b][3] = x.w;
+            }
+            if (p.counters) n_visits += dense_add<B, true>(v, warp * cols + c, n_dense, p.ids, s_ustart, s_fm, s_q, lane);
+            else dense_add<B, false>(v, warp * cols + c, n_dense, p.ids, s_ustart, s_fm, s_q, lane);
+#pragma unroll
+            for (int b = 0; b < B; ++b) *(uint4*)(acc + (size_t)b * TS + col) = make_uint4(v[b][0], v[b][1], v[b][2], v[b][3]);
+          }
+          __syncthreads();
+          phase_mark(2);
         }
       }
       // -------------------------------------------------------------------- scan + top-k (a5)
+      // warp w owns columns [w*T/NW, (w+1)*T/NW); per 128-column step every lane reads 4 scores of each row,
+      // adds the dense (bitmap) slices of the last staged chunk in registers, zero-fills, and offers keys
+      // above theta to the warp's register top-k list of that row.
       {
-        const int cols = T / kWarps;
+        const int cols = T / NW;
         const int cbase = warp * cols;
         const uint32_t gbase = (uint32_t)(p.s_id_base + t * (int64_t)T);
+        const int n_dense = s_misc[4];
+        uint64_t th[B];
 #pragma unroll
         for (int b = 0; b < B; ++b) {
-          if (b < nb) {
-            uint64_t th = own[b];
-            {
-              const uint64_t sh = *(volatile uint64_t*)&s_theta[b];
-              if (sh > th) th = sh;
+          th[b] = own[b];
+          const uint64_t sh = *(volatile uint64_t*)&s_theta[b];
+          if (sh > th[b]) th[b] = sh;
+        }
+        for (int c = 0; c < cols; c += 128) {
+          const int col = cbase + c + lane * 4;
+          uint32_t v[B][4];
+#pragma unroll
+          for (int b = 0; b < B; ++b) {
+            if (b < nb) {
+              const uint4 x = *(const uint4*)(acc + (size_t)b * TS + col);
+              *(uint4*)(acc + (size_t)b * TS + col) = make_uint4(0, 0, 0, 0);
+              v[b][0] = x.x; v[b][1] = x.y; v[b][2] = x.z; v[b][3] = x.w;
+            } else {
+              v[b][0] = v[b][1] = v[b][2] = v[b][3] = 0;
             }
-            uint32_t* row = acc + (size_t)b * TS;
-            for (int c = 0; c < cols; c += 128) {
-              const int col = cbase + c + lane * 4;
-              uint4 v = *(uint4*)(row + col);
-              *(uint4*)(row + col) = make_uint4(0, 0, 0, 0);
-              const uint32_t thh = (uint32_t)(th >> 32), thl = (uint32_t)th;
-              const uint32_t g0 = gbase + (uint32_t)col;
-              const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+          }
+          if (n_dense) {
+            if (p.counters) n_visits += dense_add<B, true>(v, cbase + c, n_dense, p.ids, s_ustart, s_fm, s_q, lane);
+            else dense_add<B, false>(v, cbase + c, n_dense, p.ids, s_ustart, s_fm, s_q, lane);
+          }
+          const uint32_t g0 = gbase + (uint32_t)col;
+#pragma unroll
+          for (int b = 0; b < B; ++b) {
+            if (b < nb) {
+              const uint32_t thh = (uint32_t)(th[b] >> 32), thl = (uint32_t)th[b];
               bool any = false;
 #pragma unroll
               for (int j = 0; j < 4; ++j)
-                any |= vv[j] > thh || (vv[j] == thh && (0xFFFFFFFFu - (g0 + j)) > thl);
+                any |= v[b][j] > thh || (v[b][j] == thh && (0xFFFFFFFFu - (g0 + j)) > thl);
               if (__any_sync(0xffffffffu, any)) {
                 {
                   const uint64_t sh = *(volatile uint64_t*)&s_theta[b];
-                  if (sh > th) th = sh;
+                  if (sh > th[b]) th[b] = sh;
                 }
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                  const uint64_t key = vv[j] ? make_key(vv[j], g0 + j) : 0;
-                  int n = list_offer_lanes<KS>(L[b], key, th, k, lane);
+                  const uint64_t key = v[b][j] ? make_key(v[b][j], g0 + j) : 0;
+                  int n = list_offer_lanes<KS>(L[b], key, th[b], k, lane);
                   n_inserts += (lane == 0) ? n : 0;
                 }
                 const uint64_t nk = list_kth<KS>(L[b], k);
@@ -423,11 +537,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_accumulate_topk(QP p) {
           }
         }
         __syncthreads();
+        phase_mark(3);
       }
     }
     // ---------------------------------------------------------------------- merge lists + finalize (a7)
     {
-      uint64_t* scratch = (uint64_t*)acc;  // [kWarps][B][k]; acc columns < T are all zero here
+      uint64_t* scratch = (uint64_t*)acc;  // [NW][B][k]; acc columns < T are all zero here
 #pragma unroll
       for (int b = 0; b < B; ++b)
 #pragma unroll
@@ -439,7 +554,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_accumulate_topk(QP p) {
 #pragma unroll
         for (int s = 0; s < KS; ++s) M[s] = 0;
         uint64_t th = kKeyFloor;
-        for (int w = 0; w < kWarps; ++w) {
+        for (int w = 0; w < NW; ++w) {
 #pragma unroll
           for (int s = 0; s < KS; ++s) {
             const int pos = s * 32 + lane;
@@ -451,8 +566,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_accumulate_topk(QP p) {
         list_finalize<KS>(M, k, r, p.inv_sigma[r], p.out_keys, p.out_ids, p.out_scores, lane);
       }
       __syncthreads();
-      for (int i = tid; i < kWarps * B * k; i += kThreads) scratch[i] = 0;
+      for (int i = tid; i < NW * B * k; i += NT_) scratch[i] = 0;
+      phase_mark(4);
     }
+  }
+  if (timing) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) atomicAdd(&p.phase[i], ph[i]);
   }
   if (p.counters) {
 #pragma unroll
@@ -472,27 +592,47 @@ struct QueryWs {
   size_t sigma_at, inv_at, runs_f_at, runs_q_at, nruns_at, counter_at, total;
 };
 
-const int kBChoices[] = {8, 6, 4, 2, 1};
+struct Shape {
+  int B, NW;
+};
 
-int pick_batch_rows(int T, int k, int requested) {
-  int KS = ks_for_k(k);
-  auto fits = [&](int B) -> bool {
-    size_t bytes = 0;
-    switch (B) {
-      case 1: bytes = Smem<1>::bytes(T, k); break;
-      case 2: bytes = Smem<2>::bytes(T, k); break;
-      case 4: bytes = Smem<4>::bytes(T, k); break;
-      case 6: bytes = Smem<6>::bytes(T, k); break;
-      case 8: bytes = Smem<8>::bytes(T, k); break;
-      default: return false;
-    }
-    if (B * KS > 24) return false;
-    return bytes <= 227 * 1024;
+bool shape_supported(int B, int NW, int KS) {
+  if (B * KS > 24 || B > NW) return false;
+  if (NW == 8) return B == 1 || B == 2 || B == 3 || B == 4;
+  if (NW == 16) return B == 1 || B == 2 || B == 4 || B == 6 || B == 8;
+  return false;
+}
+
+// pick (B rows per batch, NW warps per CTA): an explicit request must fit; auto prefers 8-warp CTAs with
+// two resident per SM (barrier stalls of one overlap the other), then 16-warp CTAs, largest B first.
+bool pick_shape(int T, int k, int req_B, int req_NW, Shape* out) {
+  const int KS = ks_for_k(k);
+  const size_t max_smem = 227 * 1024;
+  const size_t per_sm = 228 * 1024;
+  auto fits = [&](int B, int NW, int ctas) {
+    if (!shape_supported(B, NW, KS)) return false;
+    if (T % (NW * 128) != 0) return false;
+    size_t b = smem_bytes(B, T, k, NW);
+    return b <= max_smem && ctas * (b + 1024) <= per_sm;
   };
-  if (requested) return fits(requested) ? requested : -1;
-  for (int B : kBChoices)
-    if (fits(B)) return B;
-  return -1;
+  const int Bs[] = {8, 6, 4, 3, 2, 1};
+  if (req_B || req_NW) {
+    for (int NW : {8, 16}) {
+      if (req_NW && NW != req_NW) continue;
+      for (int B : Bs) {
+        if (req_B && B != req_B) continue;
+        if (fits(B, NW, 1)) { *out = {B, NW}; return true; }
+      }
+    }
+    return false;
+  }
+  for (int B : Bs)
+    if (B >= 3 && fits(B, 8, 2)) { *out = {B, 8}; return true; }
+  for (int B : Bs)
+    if (fits(B, 16, 1)) { *out = {B, 16}; return true; }
+  for (int B : Bs)
+    if (fits(B, 8, 1)) { *out = {B, 8}; return true; }
+  return false;
 }
 
 bool query_ws_layout(int64_t n_r, int64_t nnz_r, int B, QueryWs* W) {
@@ -508,26 +648,56 @@ bool query_ws_layout(int64_t n_r, int64_t nnz_r, int B, QueryWs* W) {
   return true;
 }
 
-template <int B, int KS, bool SINT8>
-cudaError_t launch_main3(const QP& p, int grid, cudaStream_t st) {
-  size_t sm = Smem<B>::bytes(p.T, p.k);
-  cudaError_t e = cudaFuncSetAttribute(k_accumulate_topk<B, KS, SINT8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+template <int B, int KS, bool SINT8, int NW>
+cudaError_t launch_main4(const QP& p, int sms, cudaStream_t st) {
+  const size_t sm = smem_bytes(B, p.T, p.k, NW);
+  auto kern = k_accumulate_topk<B, KS, SINT8, NW>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  k_accumulate_topk<B, KS, SINT8><<<grid, kThreads, sm, st>>>(p);
+  int per_sm = 1;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, sm)) != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  int64_t grid = (int64_t)sms * per_sm;
+  if (grid > p.n_batches) grid = p.n_batches;
+  kern<<<(unsigned)grid, NW * 32, sm, st>>>(p);
   return cudaGetLastError();
 }
 
-template <int B, int KS>
-cudaError_t launch_main(const QP& p, int grid, cudaStream_t st) {
-  return p.vals ? launch_main3<B, KS, true>(p, grid, st) : launch_main3<B, KS, false>(p, grid, st);
+template <int B, int KS, int NW>
+cudaError_t launch_main(const QP& p, int sms, cudaStream_t st) {
+  if constexpr (B * KS <= 24 && B <= NW) {
+    return p.vals ? launch_main4<B, KS, true, NW>(p, sms, st) : launch_main4<B, KS, false, NW>(p, sms, st);
+  } else {
+    return cudaErrorInvalidValue;
+  }
 }
 
-template <int B>
-cudaError_t launch_ks(const QP& p, int grid, cudaStream_t st) {
+template <int B, int NW>
+cudaError_t launch_ks(const QP& p, int sms, cudaStream_t st) {
   switch (ks_for_k(p.k)) {
-    case 1: return launch_main<B, 1>(p, grid, st);
-    case 4: if constexpr (B * 4 <= 24) return launch_main<B, 4>(p, grid, st); else return cudaErrorInvalidValue;
-    case 8: if constexpr (B * 8 <= 24) return launch_main<B, 8>(p, grid, st); else return cudaErrorInvalidValue;
+    case 1: return launch_main<B, 1, NW>(p, sms, st);
+    case 4: return launch_main<B, 4, NW>(p, sms, st);
+    case 8: return launch_main<B, 8, NW>(p, sms, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_shape(const Shape& sh, const QP& p, int sms, cudaStream_t st) {
+  if (sh.NW == 8) {
+    switch (sh.B) {
+      case 1: return launch_ks<1, 8>(p, sms, st);
+      case 2: return launch_ks<2, 8>(p, sms, st);
+      case 3: return launch_ks<3, 8>(p, sms, st);
+      case 4: return launch_ks<4, 8>(p, sms, st);
+    }
+  } else {
+    switch (sh.B) {
+      case 1: return launch_ks<1, 16>(p, sms, st);
+      case 2: return launch_ks<2, 16>(p, sms, st);
+      case 4: return launch_ks<4, 16>(p, sms, st);
+      case 6: return launch_ks<6, 16>(p, sms, st);
+      case 8: return launch_ks<8, 16>(p, sms, st);
+    }
   }
   return cudaErrorInvalidValue;
 }
@@ -558,10 +728,13 @@ using namespace kj;
 KJ_API size_t knnjoin_query_workspace_bytes(const knnjoin_index* idx, const knnjoin_csr* R, int32_t k,
                                             const knnjoin_query_options* qopt) {
   if (!check_query_args(idx, R, k)) return 0;
-  int B = pick_batch_rows(idx->tile, k, qopt ? qopt->batch_rows : 0);
-  if (B < 0) { set_error("no batch size fits shared memory for tile %d, k %d", idx->tile, k); return 0; }
+  Shape sh;
+  if (!pick_shape(idx->tile, k, qopt ? qopt->batch_rows : 0, qopt ? qopt->cta_warps : 0, &sh)) {
+    set_error("no (batch_rows, cta_warps) shape fits shared memory for tile %d, k %d", idx->tile, k);
+    return 0;
+  }
   QueryWs W;
-  query_ws_layout(R->n_rows, R->nnz, B, &W);
+  query_ws_layout(R->n_rows, R->nnz, sh.B, &W);
   return W.total;
 }
 
@@ -576,8 +749,13 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
     set_error("integer scores may overflow 32 bits for d = %d", idx->d);
     return KNNJOIN_ERR_UNSUPPORTED;
   }
-  int B = pick_batch_rows(idx->tile, k, qopt ? qopt->batch_rows : 0);
-  if (B < 0) { set_error("batch_rows %d unsupported for tile %d, k %d", qopt ? qopt->batch_rows : 0, idx->tile, k); return KNNJOIN_ERR_UNSUPPORTED; }
+  Shape sh;
+  if (!pick_shape(idx->tile, k, qopt ? qopt->batch_rows : 0, qopt ? qopt->cta_warps : 0, &sh)) {
+    set_error("batch_rows %d / cta_warps %d unsupported for tile %d, k %d", qopt ? qopt->batch_rows : 0,
+              qopt ? qopt->cta_warps : 0, idx->tile, k);
+    return KNNJOIN_ERR_UNSUPPORTED;
+  }
+  const int B = sh.B;
   QueryWs W;
   query_ws_layout(R->n_rows, R->nnz, B, &W);
   if (!workspace || workspace_bytes < W.total) { set_error("query workspace %zu < %zu bytes", workspace_bytes, W.total); return KNNJOIN_ERR_WORKSPACE; }
@@ -626,22 +804,15 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
   p.inv_sigma = inv_sigma;
   p.batch_counter = counter;
   p.counters = (unsigned long long*)(qopt ? qopt->counters : nullptr);
+  p.phase = (unsigned long long*)(qopt ? qopt->phase_cycles : nullptr);
   p.out_keys = out_keys;
   p.out_ids = out_ids;
   p.out_scores = out_scores;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int grid = (int)(n_batches < sms ? n_batches : sms);
   if (qopt && qopt->ev_begin) cudaEventRecord((cudaEvent_t)qopt->ev_begin, st);
-  switch (B) {
-    case 1: e = launch_ks<1>(p, grid, st); break;
-    case 2: e = launch_ks<2>(p, grid, st); break;
-    case 4: e = launch_ks<4>(p, grid, st); break;
-    case 6: e = launch_ks<6>(p, grid, st); break;
-    case 8: e = launch_ks<8>(p, grid, st); break;
-    default: e = cudaErrorInvalidValue;
-  }
+  e = launch_shape(sh, p, sms, st);
   if (qopt && qopt->ev_end) cudaEventRecord((cudaEvent_t)qopt->ev_end, st);
   if (e != cudaSuccess) return cuda_fail(e, "k_accumulate_topk");
   return KNNJOIN_OK;

@@ -35,7 +35,7 @@ def test_index_bytes_host_only():
     import paper_1011_2807_b200._binding as b
     L = b._lib
     S = b._CSR(100_000, 4_000_000, 0, 0, 0, b.BINARY)
-    opt = b._Options(8192, 0, 0.0)
+    opt = b._Options(8192, 0, 0.0, 0)
     n = L.knnjoin_index_bytes(ctypes.byref(S), 10_000, ctypes.byref(opt))
     nt = (100_000 + 8191) // 8192
     n_off = 10_000 * (nt + 1) + 1
@@ -49,6 +49,6 @@ def test_build_argument_errors(d, tile, dtype, msg):
     import paper_1011_2807_b200._binding as b
     L = b._lib
     S = b._CSR(10, 20, 0, 0, 0, dtype)
-    opt = b._Options(tile, 0, 0.0)
+    opt = b._Options(tile, 0, 0.0, 0)
     assert L.knnjoin_index_bytes(ctypes.byref(S), d, ctypes.byref(opt)) == 0
     assert msg in b.knnjoin_last_error()

@@ -146,13 +146,14 @@ def test_validate_csr():
     assert kj.knnjoin_validate_csr(oob, 8) == (3, 1)
 
 
-def test_index_layout_matches_scipy_csc():
-    """T3: decode the built index (slices per (feature, tile)) and compare with scipy's CSC per tile."""
+@pytest.mark.parametrize("name,T", [("C5", 4096), ("C2", 2048), ("C2", 8192)])
+def test_index_layout_matches_scipy_csc(name, T):
+    """T3: decode the built index (id-list and bitmap slices per (feature, tile)) and compare with scipy's CSC
+    restricted to each tile; df exact."""
     import scipy.sparse as sp
     import paper_1011_2807_b200 as kj
-    c = gen.CONFIGS["C5"].scaled(10, 9000)
+    c = gen.CONFIGS[name].scaled(10, 9000)
     S = gen.generate(c, "S")
-    T = 4096
     dS = kj.DeviceCSR.from_host(S)
     idx = kj.knnjoin_build_index(dS, c.d, tile=T)
     torch.cuda.synchronize()
@@ -160,29 +161,83 @@ def test_index_layout_matches_scipy_csc():
     raw = idx.storage.cpu().numpy()
     NT = st["n_tiles"]
     n_off = st["offsets"]
-    off = raw[:4 * n_off].view(np.uint32)
+    off_raw = raw[:4 * n_off].view(np.uint32)
+    dense_flag = (off_raw >> 31).astype(bool)
+    off = off_raw & 0x7FFFFFFF
     al = lambda x: (x + 255) // 256 * 256
     df_at = al(4 * n_off)
     df = raw[df_at:df_at + 4 * c.d].view(np.int32)
     ids_at = al(df_at + 4 * c.d)
     cap = st["unit_capacity"]
     ids = raw[ids_at:ids_at + 16 * cap].view(np.uint16)
-    vals_at = al(ids_at + 16 * cap)
-    vals = raw[vals_at:vals_at + 8 * cap].view(np.uint8)
+    words = raw[ids_at:ids_at + 16 * cap].view(np.uint32)
+    vals = None
+    if S.values is not None:
+        vals_at = al(ids_at + 16 * cap)
+        vals = raw[vals_at:vals_at + 8 * cap].view(np.uint8)
     np.testing.assert_array_equal(df, np.bincount(S.indices, minlength=c.d))
-    M = sp.csr_matrix((S.values.astype(np.int64), S.indices, S.indptr), shape=(S.n_rows, c.d)).tocsc()
-    rng = np.random.default_rng(0)
-    for f in rng.choice(c.d, 300, replace=False):
+    data = np.ones(S.nnz, np.int64) if S.values is None else S.values.astype(np.int64)
+    M = sp.csr_matrix((data, S.indices, S.indptr), shape=(S.n_rows, c.d)).tocsc()
+    n_dense = 0
+    for f in range(c.d):
         col = M[:, f]
-        rows_f = col.indices
-        vals_f = col.data
+        rows_f, vals_f = col.indices, col.data
         for t in range(NT):
-            a, b = off[f * (NT + 1) + t], off[f * (NT + 1) + t + 1]
-            got_ids = ids[8 * a:8 * b]
-            got_vals = vals[8 * a:8 * b]
-            keep = got_ids < T
-            order = np.argsort(got_ids[keep])
+            key = f * (NT + 1) + t
+            a, b = int(off[key]), int(off[key + 1])
             sel = (rows_f >= t * T) & (rows_f < (t + 1) * T)
-            np.testing.assert_array_equal(got_ids[keep][order].astype(np.int64), rows_f[sel] - t * T)
-            np.testing.assert_array_equal(got_vals[keep][order], vals_f[sel])
+            want = rows_f[sel] - t * T
+            if dense_flag[key]:
+                n_dense += 1
+                assert st["dense_min"] <= sel.sum() and b - a == T // 128
+                bits = np.unpackbits(words[4 * a:4 * b].view(np.uint8), bitorder="little")
+                np.testing.assert_array_equal(np.nonzero(bits)[0], want)
+                continue
+            got = ids[8 * a:8 * b]
+            keep = got < T
+            assert np.all(got[~keep] < T + 32)
+            order = np.argsort(got[keep])
+            np.testing.assert_array_equal(got[keep][order].astype(np.int64), want)
+            if vals is not None:
+                np.testing.assert_array_equal(vals[8 * a:8 * b][keep][order], vals_f[sel])
             assert b - a == (sel.sum() + 7) // 8
+    if name == "C2":
+        assert n_dense > 0
+    else:
+        assert n_dense == 0
+
+
+@pytest.mark.parametrize("dense_min", [-1, 0, 1, 300])
+def test_dense_bitmap_modes(dense_min):
+    """Bitmap (dense) and id-list slices give identical results; dense_min=1 forces tile/16."""
+    c = gen.CONFIGS["C2"].scaled(300, 30000)
+    R, S = gen.generate(c, "R"), gen.generate(c, "S")
+    ids, sc = _check(R, S, c.k, tile=4096, dense_min=dense_min)
+    ref = gpu_join(R, S, c.k, tile=4096, dense_min=-1)
+    np.testing.assert_array_equal(ids, ref[0])
+    np.testing.assert_array_equal(sc, ref[1])
+
+
+def test_dense_multi_chunk():
+    """More than 512 runs per batch (several staging chunks) with dense slices in non-final chunks."""
+    rng = np.random.default_rng(7)
+    d = 2000
+    rows = []
+    for _ in range(16):
+        head = list(range(0, 40))
+        tail = sorted(rng.choice(np.arange(40, d), size=400, replace=False).tolist())
+        rows.append([(f, float(np.float32(rng.lognormal()))) for f in head + tail])
+    R = csr_from_rows(rows, d, "fp32")
+    S = random_csr(rng, 6000, d, 5, 40, "binary")
+    # make the head features dense in S
+    Srows = []
+    for i in range(S.n_rows):
+        idx, _ = S.row(i)
+        extra = rng.choice(40, size=20, replace=False)
+        Srows.append(sorted(set(idx.tolist()) | set(extra.tolist())))
+    S = csr_from_rows(Srows, d, "binary")
+    cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+    _check(R, S, 10, tile=2048, batch_rows=4, counters=cnt)
+    nR = np.bincount(R.indices, minlength=d)
+    nS = np.bincount(S.indices, minlength=d)
+    assert int(cnt[0]) == int((nR.astype(np.int64) * nS).sum())
