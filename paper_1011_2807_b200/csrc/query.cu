@@ -181,11 +181,13 @@ __host__ __device__ inline size_t acc_region_bytes(int B, int T, int k, int NW) 
   return align_up(a > m ? a : m, 16);
 }
 
-// shared-memory layout of k_accumulate_topk<B, ., ., NW>; the kernel derives its pointers from the same sums
+// shared-memory layout of k_accumulate_topk<B, ., ., NW>; the kernel derives its pointers from the same sums.
+// Staging: q[kCap][QS] (QS = 4 or 8: 16-byte rows), ustart[kCap], fm[kCap], P[kCap + 1].
+__host__ __device__ constexpr int q_stride(int B) { return B <= 4 ? 4 : 8; }
 __host__ __device__ inline size_t staging_at(int B, int T, int k, int NW) { return acc_region_bytes(B, T, k, NW); }
 __host__ __device__ inline size_t tail_at(int B, int T, int k, int NW) {
-  return align_up(staging_at(B, T, k, NW) + (size_t)kCap * 4 + (size_t)(kCap + 1) * 4 + (size_t)kCap * 4 +
-                      (size_t)kCap * B * 4, 16);
+  return align_up(staging_at(B, T, k, NW) + (size_t)kCap * q_stride(B) * 4 + (size_t)kCap * 8 +
+                      (size_t)(kCap + 1) * 4, 16);
 }
 __host__ __device__ inline size_t smem_bytes(int B, int T, int k, int NW) {
   return tail_at(B, T, k, NW) + (size_t)NW * 8 /* scan partials */ + 8 * 8 /* theta_row */ + 32 /* misc */;
@@ -226,7 +228,12 @@ __device__ __forceinline__ unsigned long long dense_add(uint32_t (&v)[B][4], int
       if (e0 + u < kCap) {
         const uint32_t nib = w[u] >> sh;
         const uint32_t b0 = nib & 1u, b1 = (nib >> 1) & 1u, b2 = (nib >> 2) & 1u, b3 = (nib >> 3) & 1u;
-        const int32_t* q = s_q + (e0 + u) * B;
+        int32_t q[q_stride(B)];
+#pragma unroll
+        for (int h = 0; h < q_stride(B) / 4; ++h) {
+          const int4 q4 = *(const int4*)(s_q + (e0 + u) * q_stride(B) + 4 * h);
+          q[4 * h] = q4.x; q[4 * h + 1] = q4.y; q[4 * h + 2] = q4.z; q[4 * h + 3] = q4.w;
+        }
 #pragma unroll
         for (int b = 0; b < B; ++b) {
           const uint32_t qb = (uint32_t)q[b];
@@ -244,7 +251,7 @@ __device__ __forceinline__ unsigned long long dense_add(uint32_t (&v)[B][4], int
   return nv;
 }
 
-constexpr int kWinChunk = 4;  // 32-unit windows a warp takes per grab of the dynamic window counter
+constexpr int kWinChunk = 8;  // 32-unit windows a warp takes per grab of the dynamic window counter
 
 template <int B, int KS, bool SINT8, int NW>
 __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
@@ -255,10 +262,11 @@ __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
   const int TS = acc_stride(T);
   uint32_t* acc = (uint32_t*)smem;
   const uint32_t acc_s = (uint32_t)__cvta_generic_to_shared(acc);
-  uint32_t* s_ustart = (uint32_t*)(smem + staging_at(B, T, p.k, NW));
-  uint32_t* s_P = s_ustart + kCap;
-  uint32_t* s_fm = s_P + kCap + 1;
-  int32_t* s_q = (int32_t*)(s_fm + kCap);
+  constexpr int QS = q_stride(B);
+  int32_t* s_q = (int32_t*)(smem + staging_at(B, T, p.k, NW));
+  uint32_t* s_ustart = (uint32_t*)(s_q + kCap * QS);
+  uint32_t* s_fm = s_ustart + kCap;
+  uint32_t* s_P = s_fm + kCap;
   uint64_t* s_warp = (uint64_t*)(smem + tail_at(B, T, p.k, NW));
   uint64_t* s_theta = s_warp + NW;
   int* s_misc = (int*)(s_theta + 8);  // [0] batch, [1] n sparse items, [2] TOT, [3] window counter, [4] n dense
@@ -341,7 +349,7 @@ __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
               s_fm[c] = fm[it];
               const size_t run = (size_t)(run_base + c0 + tid * IPT + it);
 #pragma unroll
-              for (int b = 0; b < B; ++b) s_q[c * B + b] = p.runs_q[run * B + b];
+              for (int b = 0; b < B; ++b) s_q[c * QS + b] = p.runs_q[run * B + b];
             }
             ex += pk[it];
           }
@@ -373,29 +381,26 @@ __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
               if (s_P[mid] <= p_begin) lo = mid; else hi = mid - 1;
             }
             int e_cur = lo;
+            // lane l takes unit p0 + l.  e_cur is the item covering p0; the items starting inside the window
+            // are found with one OR-reduction of their start offsets (starts are strictly increasing).
             auto lookup = [&](uint32_t p0, int& e_out, uint32_t& unit, bool& valid) {
               const uint32_t nxt = s_P[e_cur + 1];
-              int e = e_cur;
+              int e = e_cur, e_next;
               if (p0 + 32 > nxt) {
                 const int j = min(e_cur + 1 + lane, n_items);
-                const uint32_t o = s_P[j];
-                const uint32_t pp = p0 + lane;
-                int cc = 0;
-#pragma unroll
-                for (int st = 16; st; st >>= 1) {
-                  uint32_t v = __shfl_sync(0xffffffffu, o, cc + st - 1);
-                  if (v <= pp) cc += st;
-                }
-                e = e_cur + cc;
+                const uint32_t o = s_P[j] - p0;  // >= 1
+                const uint32_t M = __reduce_or_sync(0xffffffffu, o < 32 ? (1u << o) : 0u);
+                e = e_cur + __popc(M & (0xFFFFFFFFu >> (31 - lane)));
+                e_next = e_cur + __popc(M) + (__ballot_sync(0xffffffffu, o == 32) ? 1 : 0);
+              } else {
+                e_next = e_cur + (nxt == p0 + 32 ? 1 : 0);
               }
               const uint32_t pp = p0 + lane;
               valid = pp < p_end;
               if (!valid) e = e_cur;
               e_out = e;
               unit = s_ustart[e] + (pp - s_P[e]);
-              const int e31 = __shfl_sync(0xffffffffu, e, 31);
-              e_cur = e31 + (s_P[e31 + 1] <= p0 + 32 ? 1 : 0);
-              if (e_cur > n_items - 1) e_cur = n_items - 1;
+              e_cur = min(e_next, n_items - 1);
             };
             int eA;
             uint32_t uA;
@@ -432,7 +437,7 @@ __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
 #pragma unroll
                 for (int b = 0; b < B; ++b) {
                   if (mask & (1u << b)) {
-                    const uint32_t q = (uint32_t)s_q[eA * B + b];
+                    const uint32_t q = (uint32_t)s_q[eA * QS + b];
                     const uint32_t rb = acc_s + (uint32_t)(b * TS * 4);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
