@@ -217,6 +217,7 @@ def bench_ours(args):
     import torch.distributed as dist
 
     import paper_1011_2807_b200 as kj
+    from paper_1011_2807_b200 import dist as kdist
 
     rank, world, local = dist_env()
     if world != args.gpus:
@@ -247,8 +248,7 @@ def bench_ours(args):
             return ids, sc
         _, _, keys = kj.knnjoin_query(idx, dR_, k, want_keys=True, want_ids=False, batch_rows=args.batch_rows,
                                       events=kernel_events, cta_warps=args.cta_warps)
-        gathered = torch.empty((world,) + tuple(keys.shape), dtype=keys.dtype, device=dev)
-        dist.all_gather_into_tensor(gathered, keys)
+        gathered = kdist.all_gather_keys(keys)  # one NCCL all_gather_into_tensor over NVLink
         ids, sc, _ = kj.knnjoin_merge(gathered, dR_, d, dS_.dtype, k)
         return ids, sc
 
