@@ -45,7 +45,8 @@ def parse():
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--batch-rows", type=int, default=0)
     ap.add_argument("--cta-warps", type=int, default=0)
-    ap.add_argument("--dense-min", type=int, default=0, help="0 auto (tile/4), -1 never, >0 postings per bitmap slice")
+    ap.add_argument("--head-density", type=float, default=0.0, help="0 auto (1/8), <0 no head features")
+    ap.add_argument("--head-max", type=int, default=0, help="0 auto (64)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -241,7 +242,7 @@ def bench_ours(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def step(dS_, dR_, kernel_events=None):
-        idx = kj.knnjoin_build_index(dS_, d, s_id_base=s_base, tile=args.tile, dense_min=args.dense_min)
+        idx = kj.knnjoin_build_index(dS_, d, s_id_base=s_base, tile=args.tile, head_density=args.head_density, head_max=args.head_max)
         if world == 1:
             ids, sc, _ = kj.knnjoin_query(idx, dR_, k, batch_rows=args.batch_rows, events=kernel_events,
                                           cta_warps=args.cta_warps)
@@ -271,13 +272,13 @@ def bench_ours(args):
 
     # per-phase SM cycles of the accumulate kernel (one untimed instrumented step)
     phase = torch.zeros(8, dtype=torch.int64, device=dev)
-    idx_p = kj.knnjoin_build_index(dS, d, s_id_base=s_base, tile=args.tile, dense_min=args.dense_min)
+    idx_p = kj.knnjoin_build_index(dS, d, s_id_base=s_base, tile=args.tile, head_density=args.head_density, head_max=args.head_max)
     kj.knnjoin_query(idx_p, dR, k, batch_rows=args.batch_rows, phase_cycles=phase, cta_warps=args.cta_warps)
     torch.cuda.synchronize()
     ph = phase.cpu().tolist()
     tot_ph = max(1, sum(ph[:6]))
     phase_share = {n: round(ph[i] / tot_ph, 4) for i, n in
-                   enumerate(["staging", "sparse_atomics", "dense_pass", "scan_topk", "merge_output", "batch_setup"])}
+                   enumerate(["staging", "sparse_atomics", "unused", "scan_topk", "merge_output", "batch_setup_head_tables"])}
     del idx_p
 
     def timed_region():
@@ -370,7 +371,7 @@ def bench_ours(args):
     peak, peak_src = measured_peak()
     achieved = V * b_post / (kern_avg_max * 1e-3) / 1e9
     stats = kj.knnjoin_index_stats(kj.knnjoin_build_index(dS, d, s_id_base=s_base, tile=args.tile,
-                                                          dense_min=args.dense_min))
+                                                          head_density=args.head_density, head_max=args.head_max))
     props = torch.cuda.get_device_properties(dev)
     out = {
         "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
@@ -380,7 +381,7 @@ def bench_ours(args):
                    "R_rows": R.n_rows, "S_rows_per_gpu": n_s, "S_rows_total": n_s * world,
                    "nnz_R": int(R.nnz), "nnz_S_per_gpu": int(S.nnz), "tile": stats["tile"],
                    "n_tiles": stats["n_tiles"], "batch_rows": args.batch_rows or "auto",
-                   "dense_min": stats["dense_min"],
+                   "head_min_df": stats["head_min_df"], "head_max": stats["head_max"],
                    "step": "knnjoin_build_index(S) + knnjoin_query(R,k)" + (" + all_gather + knnjoin_merge" if world > 1 else ""),
                    "l2": "flushed before every timed step (256 MiB write, outside the step's events)",
                    "parallelism": f"S-sharded x{world}" if world > 1 else "1 GPU",

@@ -62,16 +62,17 @@ typedef struct {
 /* Build options.  tile: S ids per tile (the S-block of Alg. 1 mapped to a shared-memory score array);
  * 0 = default 8192; must be a multiple of 2048 and <= 32768.
  * prune / alpha: reserved for the threshold-pruned mode; must be 0 / 0.
- * dense_min: encoding of dense slices (BINARY S only).  A slice (I_f restricted to one tile) with at least
- *   dense_min postings is stored as a tile-wide bitmap (tile/8 bytes) instead of a list of local ids, and
- *   its scores are accumulated in registers during the top-k scan instead of by shared-memory atomics.
- *   0 = default (tile/4 postings, i.e. density >= 1/4); -1 = never (every slice is an id list).  Values
- *   below tile/16 are raised to tile/16 (a bitmap is then never larger than the id list it replaces). */
+ * head_density / head_max: "head features" (BINARY S only).  Up to head_max (0 = 64, at most 64) of the
+ *   most frequent features with df >= head_density * |S| (0 = default 1/8, negative = no head features) are
+ *   not stored as id lists: each S row gets one 64-bit word of head-feature bits, and the query adds their
+ *   contributions from per-batch lookup tables (4 features per 16-entry table) during the top-k scan instead
+ *   of one shared-memory atomic per posting.  Same integer sums, different encoding of I_d. */
 typedef struct {
   int32_t tile;
   int32_t prune;
   float alpha;
-  int32_t dense_min;
+  float head_density;
+  int32_t head_max;
 } knnjoin_options;
 
 /* Query options (all optional; pass NULL for defaults).
@@ -84,7 +85,7 @@ typedef struct {
  *  ev_begin / ev_end: NULL, or cudaEvent_t (as void*) recorded on `stream` immediately before and after
  *              the score-accumulation + top-k kernel, so callers can time that kernel alone.
  *  phase_cycles: NULL, or a device int64_t[8] that the query ADDS SM clock cycles into, summed over CTAs
- *              (thread 0 of each CTA): [0] staging, [1] sparse atomics, [2] dense pass, [3] scan + top-k,
+ *              (thread 0 of each CTA): [0] staging, [1] sparse atomics, [2] head tables, [3] scan + top-k,
  *              [4] list merge + output, [5] batch fetch / setup.  Profiling aid; off when NULL. */
 typedef struct {
   int32_t batch_rows;
@@ -107,7 +108,8 @@ typedef struct {
   int64_t unit_capacity;/* 16-byte posting units reserved in the storage (upper bound) */
   int64_t storage_bytes;/* bytes of index storage the handle uses */
   knnjoin_dtype s_dtype;
-  int32_t dense_min;    /* postings per slice from which a slice is a bitmap (INT32_MAX = never) */
+  int64_t head_min_df;  /* df from which a feature may be a head feature (-1: head features off) */
+  int32_t head_max;     /* cap on the number of head features (their count is known on the device only) */
 } knnjoin_index_info;
 
 /* ---- index build: Create_Inverted_List_IIB (Alg. 3 lines 5-8) on the device ------ */
@@ -123,8 +125,9 @@ size_t knnjoin_build_workspace_bytes(const knnjoin_csr* S, int32_t d, const knnj
  * aligned) using `workspace` (>= knnjoin_build_workspace_bytes bytes).  Layout:
  * for tile t (S ids [t*tile, (t+1)*tile)) and feature f, the postings of I_f restricted to the tile are a
  * contiguous, 16-byte aligned slice of local ids (+ uint8 values for INT8 S), padded with dummy ids
- * tile + (0..31), permuted inside each 256-posting block so a warp's 32 lanes touch consecutive ids;
- * dense slices (see dense_min) are tile-wide bitmaps, flagged by bit 31 of their start offset.
+ * tile + (0..31); inside each full 256-posting block postings are ordered by shared-memory bank, the last
+ * partial block is transposed so a warp's lanes touch consecutive ids; head features (see head_density)
+ * are stored as one 64-bit word per S row instead of id lists.
  * s_id_base: global id of S row 0 (ids returned by queries are s_id_base + local row).
  * S may be freed after the call's work completes on `stream`; the storage must outlive every query.
  * S dtype must be BINARY or INT8 (FP32 S -> KNNJOIN_ERR_UNSUPPORTED).  *out receives a host handle

@@ -32,7 +32,7 @@ class _CSR(ctypes.Structure):
 
 class _Options(ctypes.Structure):
     _fields_ = [("tile", ctypes.c_int32), ("prune", ctypes.c_int32), ("alpha", ctypes.c_float),
-                ("dense_min", ctypes.c_int32)]
+                ("head_density", ctypes.c_float), ("head_max", ctypes.c_int32)]
 
 
 class _QueryOptions(ctypes.Structure):
@@ -44,7 +44,7 @@ class _IndexInfo(ctypes.Structure):
     _fields_ = [("n_s", ctypes.c_int64), ("s_id_base", ctypes.c_int64), ("d", ctypes.c_int32),
                 ("tile", ctypes.c_int32), ("n_tiles", ctypes.c_int64), ("offsets", ctypes.c_int64),
                 ("unit_capacity", ctypes.c_int64), ("storage_bytes", ctypes.c_int64), ("s_dtype", ctypes.c_int),
-                ("dense_min", ctypes.c_int32)]
+                ("head_min_df", ctypes.c_int64), ("head_max", ctypes.c_int32)]
 
 
 def library_path() -> str:
@@ -182,9 +182,10 @@ def _empty_u8(nbytes: int, device) -> torch.Tensor:
 
 
 def knnjoin_build_index(S: DeviceCSR, d: int, s_id_base: int = 0, tile: int = 0, stream=None,
-                        workspace: torch.Tensor | None = None, dense_min: int = 0) -> Index:
+                        workspace: torch.Tensor | None = None, head_density: float = 0.0,
+                        head_max: int = 0) -> Index:
     cS = S._c()
-    opt = _Options(tile, 0, 0.0, dense_min)
+    opt = _Options(tile, 0, 0.0, head_density, head_max)
     nbytes = _lib.knnjoin_index_bytes(ctypes.byref(cS), d, ctypes.byref(opt))
     if nbytes == 0:
         raise KnnJoinError(1, "knnjoin_index_bytes", knnjoin_last_error())

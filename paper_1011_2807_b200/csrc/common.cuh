@@ -15,13 +15,12 @@ namespace kj {
 
 constexpr int kWarps = 16;             // warps per CTA of the accumulation kernel
 constexpr int kThreads = kWarps * 32;  // 512
-constexpr int kCap = kThreads;         // posting runs staged in shared memory per chunk (one per thread)
 constexpr int kMaxK = 256;
 constexpr int kDefaultTile = 8192;
 constexpr int kMaxTile = 32768;        // local ids < tile; padding ids are tile + (0..31) (dummy columns)
 constexpr int kTileQuantum = 2048;     // tile must split into kWarps column strips of 128-column chunks
-constexpr uint32_t kDenseFlag = 0x80000000u;
-constexpr uint32_t kOffMask = 0x7FFFFFFFu;
+constexpr int kMaxHead = 64;                  // head features per index (one 64-bit word per S row)
+constexpr float kDefaultHeadDensity = 0.125f;  // df >= |S|/8 makes a feature a head candidate
 constexpr int kPadCols = 32;           // dummy score columns per row that absorb padding postings
 constexpr uint64_t kKeyFloor = 0x00000000FFFFFFFFull;  // score 0 with every id: admits nothing
 constexpr double kFixedOne = 1073741824.0;              // 2^30: per-row fixed-point scale numerator
@@ -34,7 +33,8 @@ __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a -
 // host-side layout of the index storage (all offsets 256-byte aligned)
 struct IndexLayout {
   int64_t n_tiles = 0, n_off = 0, unit_cap = 0;
-  size_t off_at = 0, df_at = 0, ids_at = 0, vals_at = 0, total = 0;
+  size_t off_at = 0, df_at = 0, head_slot_at = 0, head_feat_at = 0, head_cols_at = 0, ids_at = 0, vals_at = 0,
+         total = 0;
 };
 bool index_layout(const knnjoin_csr* S, int32_t d, int32_t tile, IndexLayout* L);
 int32_t resolve_tile(const knnjoin_options* opt);
@@ -54,11 +54,14 @@ struct knnjoin_index {
   int32_t d = 0, tile = 0;
   int64_t n_tiles = 0, n_off = 0, unit_cap = 0;
   knnjoin_dtype s_dtype = KNNJOIN_BINARY;
-  int32_t dense_min = 0x7FFFFFFF;  // slices with >= dense_min postings are tile-wide bitmaps
-  const uint32_t* off = nullptr;  // [n_off] posting-unit (16 B) offsets, feature-major: f*(n_tiles+1)+t;
-                                  // bit 31 set: the slice starting here is a bitmap (tile/128 units)
-  const int32_t* df = nullptr;    // [d] |I_d| (document frequency of each feature in S)
-  const uint16_t* ids = nullptr;  // [unit_cap*8] local S ids (< tile); padding = tile + (u mod 32)
-  const uint8_t* vals = nullptr;  // [unit_cap*8] INT8 S weights (nullptr for BINARY S)
+  uint32_t head_min_df = 0xFFFFFFFFu;  // df threshold of head features (0xFFFFFFFF: none)
+  int32_t head_max = 0;                // cap on head features (0: none)
+  const uint32_t* off = nullptr;       // [n_off] posting-unit (16 B) offsets, feature-major: f*(n_tiles+1)+t
+  const int32_t* df = nullptr;         // [d] |I_d| (document frequency of each feature in S)
+  const int32_t* head_slot = nullptr;  // [d] head slot of a feature, -1 if not a head feature
+  const int32_t* head_feat = nullptr;  // [kMaxHead + 1] feature of each head slot (-1 unused); [kMaxHead] = n_head
+  const uint64_t* head_cols = nullptr; // [n_tiles * tile] bit i: S row has head feature head_feat[i]
+  const uint16_t* ids = nullptr;       // [unit_cap*8] local S ids (< tile); padding = tile + (u mod 32)
+  const uint8_t* vals = nullptr;       // [unit_cap*8] INT8 S weights (nullptr for BINARY S)
   size_t storage_bytes = 0;
 };

@@ -1,7 +1,7 @@
 // index_build.cu -- K1: the tiled inverted index of S, built on the device.
 //
 // This is Create_Inverted_List_IIB (Alg. 3 lines 5-8: "for every feature (d, w) of
-// every s insert (s, w) into I_d") re-shaped for the GPU: the lists are partitioned into S-id tiles of
+// every s insert (s, w) into I_d") re-shaped for the GPU.  The lists are partitioned into S-id tiles of
 // `tile` ids (the analogue of Alg. 1's S blocks, sized so one tile's score array fits in shared memory)
 // and laid out feature-major so that slice (f, t) = I_f ∩ tile t is contiguous:
 //
@@ -10,20 +10,25 @@
 //                                                            entries hold tile + (u mod 32), a dummy column
 //   vals[8*u .. 8*u+8)                                       INT8 S weights (same positions)
 //
+// Head features.  For BINARY S, the (up to 64) most frequent features with df >= head_density * |S| are
+// not stored as id lists at all: every S row s gets a 64-bit word head_cols[s] whose bit i says "s has
+// head feature head_feat[i]".  The query accumulates them from per-batch lookup tables (Four Russians,
+// 4 features per table) instead of one shared-memory atomic per posting.
+//
 // Steps (all stream-ordered, integer, deterministic, no contended atomics -- Zipf head features put every
 // row of a tile on the same key, so a global-atomic histogram would serialise):
 //   1. k_keys      key(s, f) = f*(n_tiles+1) + t(s) for every nonzero, value = (local id, weight)
 //   2. CUB stable radix sort of (key, value) pairs -- CSR order is ascending s, so each key's postings come
 //      out in ascending s (Alg. 3 inserts "in B_s scan order")
 //   3. k_seg_first / k_seg_count: run-length of equal keys -> first[key], counts[key]; k_df: df[f] = |I_f|
-//   4. k_units     units(key) = ceil(count/8) (16-byte alignment), or tile/128 for a bitmap slice;
-//      CUB exclusive scan: off = scan(units)
-//   5. k_scatter   posting of sorted rank rho inside slice goes to block rho/256, and inside a block of m
-//      units to lane i = rho%m, slot j = rho/m (unit i holds sorted postings i, i+m, ..., i+7m): when a
-//      warp's lane i loads unit i and issues atomic j, the 32 lanes hit 32 consecutive ids of a dense
-//      slice -> 32 distinct shared-memory banks.
-//      Dense slices (>= dense_min postings, BINARY S) are instead a tile-wide bitmap (bit = local id).
-//   6. k_mark_dense sets bit 31 of a dense slice's start offset.
+//   4. head selection: CUB descending sort of (df, f) over the d features, k_head_select
+//   5. k_units: units(key) = ceil(count/8) (0 for head features); CUB exclusive scan: off = scan(units)
+//   6. k_fill_pads, k_scatter (posting of sorted rank rho at position rho of its slice), k_block_layout:
+//      inside every full 256-posting block (32 units) the postings are ordered by shared-memory bank
+//      (id mod 32), so slot j of the 32 units holds postings of ~32 distinct banks; the final partial block
+//      of m units is transposed (unit i holds sorted postings i, i+m, ..., i+7m) so the lanes of a warp hit
+//      consecutive ids
+//   7. k_head_cols: one 64-bit head word per S row.
 // The paper counts this as Eq. 4's first term, sum |s_i| postings.
 #include <cub/cub.cuh>
 
@@ -49,6 +54,12 @@ bool index_layout(const knnjoin_csr* S, int32_t d, int32_t tile, IndexLayout* L)
   at = align_up(at + sizeof(uint32_t) * (size_t)L->n_off, 256);
   L->df_at = at;
   at = align_up(at + sizeof(int32_t) * (size_t)d, 256);
+  L->head_slot_at = at;
+  at = align_up(at + sizeof(int32_t) * (size_t)d, 256);
+  L->head_feat_at = at;
+  at = align_up(at + sizeof(int32_t) * (kMaxHead + 1), 256);  // [kMaxHead] features + n_head
+  L->head_cols_at = at;
+  at = align_up(at + sizeof(uint64_t) * (size_t)L->n_tiles * tile, 256);
   L->ids_at = at;
   at = align_up(at + 16 * (size_t)L->unit_cap, 256);
   L->vals_at = at;
@@ -57,20 +68,11 @@ bool index_layout(const knnjoin_csr* S, int32_t d, int32_t tile, IndexLayout* L)
   return true;
 }
 
-// postings from which a slice is stored as a bitmap (0xFFFFFFFF = never); BINARY S only
-uint32_t dense_threshold(const knnjoin_csr* S, int32_t tile, const knnjoin_options* opt) {
-  if (S->dtype != KNNJOIN_BINARY) return 0xFFFFFFFFu;
-  int32_t v = opt ? opt->dense_min : 0;
-  if (v < 0) return 0xFFFFFFFFu;
-  if (v == 0) v = tile / 4;
-  if (v < tile / 16) v = tile / 16;
-  return (uint32_t)v;
-}
-
 namespace {
 
 struct BuildWs {
-  size_t counts_at, units_at, first_at, ka_at, kb_at, va_at, vb_at, cub_at, cub_bytes, total;
+  size_t counts_at, units_at, first_at, ka_at, kb_at, va_at, vb_at, dfk_at, dfk2_at, fv_at, fv2_at, cub_at,
+      cub_bytes, total;
 };
 
 int end_bit_for(int64_t max_key) {
@@ -79,14 +81,17 @@ int end_bit_for(int64_t max_key) {
   return b;
 }
 
-bool build_ws_layout(const knnjoin_csr* S, const IndexLayout& L, BuildWs* W) {
+bool build_ws_layout(const knnjoin_csr* S, int32_t d, const IndexLayout& L, BuildWs* W) {
   size_t nnz = (size_t)S->nnz, n_off = (size_t)L.n_off;
-  size_t sort_bytes = 0, scan_bytes = 0;
+  size_t sort_bytes = 0, scan_bytes = 0, dsort_bytes = 0;
   cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
                                                   (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)nnz, 0,
                                                   end_bit_for(L.n_off - 1));
   if (e != cudaSuccess) return false;
   e = cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n_off);
+  if (e != cudaSuccess) return false;
+  e = cub::DeviceRadixSort::SortPairsDescending(nullptr, dsort_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                                (const int32_t*)nullptr, (int32_t*)nullptr, d);
   if (e != cudaSuccess) return false;
   size_t at = 0;
   W->counts_at = at; at = align_up(at + 4 * n_off, 256);
@@ -96,8 +101,14 @@ bool build_ws_layout(const knnjoin_csr* S, const IndexLayout& L, BuildWs* W) {
   W->kb_at = at;     at = align_up(at + 4 * nnz, 256);
   W->va_at = at;     at = align_up(at + 4 * nnz, 256);
   W->vb_at = at;     at = align_up(at + 4 * nnz, 256);
+  W->dfk_at = at;    at = align_up(at + 4 * (size_t)d, 256);
+  W->dfk2_at = at;   at = align_up(at + 4 * (size_t)d, 256);
+  W->fv_at = at;     at = align_up(at + 4 * (size_t)d, 256);
+  W->fv2_at = at;    at = align_up(at + 4 * (size_t)d, 256);
   W->cub_at = at;
-  W->cub_bytes = sort_bytes > scan_bytes ? sort_bytes : scan_bytes;
+  W->cub_bytes = sort_bytes;
+  if (scan_bytes > W->cub_bytes) W->cub_bytes = scan_bytes;
+  if (dsort_bytes > W->cub_bytes) W->cub_bytes = dsort_bytes;
   at = align_up(at + W->cub_bytes, 256);
   W->total = at;
   return true;
@@ -116,6 +127,7 @@ bool check_build_args(const knnjoin_csr* S, int32_t d, const knnjoin_options* op
   *tile = resolve_tile(opt);
   if (*tile < 0) { set_error("tile must be a multiple of %d in [%d, %d]", kTileQuantum, kTileQuantum, kMaxTile); return false; }
   if (opt && (opt->prune != 0)) { set_error("pruned mode is not available in this build (options.prune must be 0)"); return false; }
+  if (opt && opt->head_max > kMaxHead) { set_error("head_max must be <= %d", kMaxHead); return false; }
   if ((int64_t)d * ((S->n_rows + *tile - 1) / *tile + 1) + 1 >= ((int64_t)1 << 31)) {
     set_error("d * (n_tiles+1) too large for 32-bit slice keys; shard S or raise the tile width");
     return false;
@@ -162,8 +174,9 @@ __global__ void k_seg_count(const uint32_t* __restrict__ keys, int64_t nnz, uint
   if (k < sentinel_key && (i == nnz - 1 || keys[i + 1] != k)) counts[k] = (uint32_t)(i + 1) - first[k];
 }
 
-// warp per feature: df[f] = sum over tiles of counts[f][t]
-__global__ void k_df(const uint32_t* __restrict__ counts, int32_t d, int64_t n_tiles, int32_t* __restrict__ df) {
+// warp per feature: df[f] = sum over tiles of counts[f][t]; also the (df, f) pairs for head selection
+__global__ void k_df(const uint32_t* __restrict__ counts, int32_t d, int64_t n_tiles, int32_t* __restrict__ df,
+                     uint32_t* __restrict__ dfk, int32_t* __restrict__ fv) {
   int64_t f = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (f >= d) return;
@@ -171,7 +184,42 @@ __global__ void k_df(const uint32_t* __restrict__ counts, int32_t d, int64_t n_t
   for (int64_t t = lane; t < n_tiles; t += 32) s += counts[f * (n_tiles + 1) + t];
 #pragma unroll
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) df[f] = (int32_t)s;
+  if (lane == 0) {
+    df[f] = (int32_t)s;
+    dfk[f] = s;
+    fv[f] = (int32_t)f;
+  }
+}
+
+// one warp: the first head_max features of the (df desc, f asc) order with df >= min_df become heads
+__global__ void k_head_select(const uint32_t* __restrict__ dfk_sorted, const int32_t* __restrict__ f_sorted,
+                              int32_t d, uint32_t min_df, int32_t head_max, int32_t* __restrict__ head_slot,
+                              int32_t* __restrict__ head_feat) {
+  const int lane = threadIdx.x;
+  int n = 0;
+  for (int base = 0; base < kMaxHead; base += 32) {
+    const int i = base + lane;
+    const bool take = i < head_max && i < d && dfk_sorted[i] >= min_df && dfk_sorted[i] > 0;
+    const uint32_t m = __ballot_sync(0xffffffffu, take);
+    if (take) {
+      head_feat[i] = f_sorted[i];
+      head_slot[f_sorted[i]] = i;
+    } else {
+      head_feat[i] = -1;
+    }
+    n += __popc(m);
+  }
+  if (lane == 0) head_feat[kMaxHead] = n;  // n_head (heads are a prefix: df is sorted)
+}
+
+__global__ void k_units(const uint32_t* __restrict__ counts, uint32_t* __restrict__ units, int64_t n,
+                        int64_t n_tiles, const int32_t* __restrict__ head_slot) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t c = counts[i];
+  uint32_t u = (c + 7u) >> 3;
+  if (c && head_slot[i / (n_tiles + 1)] >= 0) u = 0;  // head features live in head_cols, not in id lists
+  units[i] = u;
 }
 
 // padding entries point at one of 32 dummy score columns [tile, tile+32) (spread over banks by unit index),
@@ -184,57 +232,144 @@ __global__ void k_fill_pads(uint4* __restrict__ ids, int64_t units, uint32_t til
   ids[u] = make_uint4(pad, pad, pad, pad);
 }
 
-__global__ void k_units(const uint32_t* __restrict__ counts, uint32_t* __restrict__ units, int64_t n,
-                        uint32_t dense_min, uint32_t dense_units) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) {
-    uint32_t c = counts[i];
-    units[i] = c >= dense_min ? dense_units : (c + 7u) >> 3;
-  }
-}
-
-// zero the bitmap of every dense slice (the pad fill wrote dummy ids there)
-__global__ void k_zero_dense(const uint32_t* __restrict__ counts, const uint32_t* __restrict__ off, int64_t n,
-                             uint32_t dense_min, uint32_t dense_units, uint4* __restrict__ ids) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n || counts[i] < dense_min) return;
-  uint4* b = ids + off[i];
-  for (uint32_t u = 0; u < dense_units; ++u) b[u] = make_uint4(0, 0, 0, 0);
-}
-
-__global__ void k_mark_dense(const uint32_t* __restrict__ counts, uint32_t* __restrict__ off, int64_t n,
-                             uint32_t dense_min) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n && counts[i] >= dense_min) off[i] |= kDenseFlag;
-}
-
+// posting of sorted rank rho goes to position rho of its slice (k_block_layout permutes inside blocks)
 __global__ void k_scatter(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, int64_t nnz,
                           const uint32_t* __restrict__ off, const uint32_t* __restrict__ first,
-                          const uint32_t* __restrict__ counts, uint32_t dense_min, uint32_t sentinel_key,
-                          uint16_t* __restrict__ ids, uint8_t* __restrict__ wvals) {
+                          const uint32_t* __restrict__ units, uint32_t sentinel_key, uint16_t* __restrict__ ids,
+                          uint8_t* __restrict__ wvals) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nnz) return;
   uint32_t key = keys[i];
-  if (key >= sentinel_key) return;
-  uint32_t u0 = off[key];
-  if (counts[key] >= dense_min) {  // bitmap slice: bit `local id`
-    uint32_t local = vals[i] & 0xFFFFu;
-    atomicOr((uint32_t*)ids + (size_t)u0 * 4 + (local >> 5), 1u << (local & 31));
-    return;
-  }
-  uint32_t rank = (uint32_t)i - first[key];
-  uint32_t U = off[key + 1] - u0;
-  uint32_t beta = rank >> 8, iota = rank & 255u;
-  uint32_t m = U - 32u * beta;
-  if (m > 32u) m = 32u;
-  uint32_t ii = iota % m, jj = iota / m;
-  size_t pos = (size_t)u0 * 8 + (size_t)beta * 256 + ii * 8 + jj;
-  uint32_t v = vals[i];
+  if (key >= sentinel_key || units[key] == 0) return;  // invalid feature or head feature
+  const size_t pos = (size_t)off[key] * 8 + ((uint32_t)i - first[key]);
+  const uint32_t v = vals[i];
   ids[pos] = (uint16_t)(v & 0xFFFFu);
   if (wvals) wvals[pos] = (uint8_t)(v >> 16);
 }
 
+// Warp per slice (grid-stride over keys).  Full 256-posting blocks: stable counting sort by bank
+// (id mod 32; padding last): rank r -> position r (unit r/8, slot r%8).  Final partial block of m units:
+// transpose (unit i holds sorted postings i, i+m, ...).  Deterministic: ranks come from slot-ordered
+// match_any passes, not from the order of atomics.
+__global__ void k_block_layout(const uint32_t* __restrict__ off, const uint32_t* __restrict__ units, int64_t n_keys,
+                               uint32_t tile, uint16_t* __restrict__ ids, uint8_t* __restrict__ wvals) {
+  __shared__ uint32_t s_cnt[8][33];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint32_t* cnt = s_cnt[wib];
+  const uint32_t lt = (1u << lane) - 1u;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t key = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; key < n_keys; key += nwarps) {
+    const uint32_t U = units[key];
+    if (U == 0) continue;
+    const size_t base = (size_t)off[key] * 8;
+    const uint32_t nblk = (U + 31) / 32;
+    for (uint32_t blk = 0; blk < nblk; ++blk) {
+      const uint32_t m = min(32u, U - 32u * blk);
+      const size_t b0 = base + (size_t)blk * 256;
+      uint16_t id[8];
+      uint8_t w[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { id[j] = 0xFFFF; w[j] = 0; }
+      if (lane < (int)m) {
+        const uint4 x = *(const uint4*)(ids + b0 + 8 * lane);
+        const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) id[j] = (uint16_t)(xs[j >> 1] >> (16 * (j & 1)));
+        if (wvals) {
+          const uint2 y = *(const uint2*)(wvals + b0 + 8 * lane);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) w[j] = (uint8_t)((j < 4 ? y.x : y.y) >> (8 * (j & 3)));
+        }
+      }
+      uint32_t dst[8];
+      if (m == 32) {
+        cnt[lane] = 0;
+        if (lane == 0) cnt[32] = 0;
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {  // bucket sizes (bucket 32 = padding)
+          const uint32_t bk = id[j] >= tile ? 32u : (id[j] & 31u);
+          const uint32_t peers = __match_any_sync(0xffffffffu, bk);
+          if ((peers & lt) == 0) cnt[bk] += __popc(peers);
+          __syncwarp();
+        }
+        const uint32_t c = cnt[lane];
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        __syncwarp();
+        cnt[lane] = incl - c;
+        if (lane == 31) cnt[32] = incl;  // padding after every real posting
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {  // ranks in (slot, lane) order within each bucket
+          const uint32_t bk = id[j] >= tile ? 32u : (id[j] & 31u);
+          const uint32_t peers = __match_any_sync(0xffffffffu, bk);
+          const uint32_t start = cnt[bk];
+          dst[j] = start + __popc(peers & lt);
+          __syncwarp();
+          if ((peers & lt) == 0) cnt[bk] = start + __popc(peers);
+          __syncwarp();
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {  // plain position p = 8*lane + j -> unit p % m, slot p / m
+          const uint32_t p = 8u * lane + j;
+          dst[j] = (p % m) * 8 + p / m;
+        }
+      }
+      __syncwarp();
+      if (lane < (int)m) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          ids[b0 + dst[j]] = id[j];
+          if (wvals) wvals[b0 + dst[j]] = w[j];
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// warp per S row: bit i of head_cols[row] <=> row has head feature head_feat[i]; tail columns of the last
+// tile stay 0 (memset)
+__global__ void k_head_cols(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices, int64_t n_s,
+                            int32_t d, const int32_t* __restrict__ head_slot, uint64_t* __restrict__ cols) {
+  int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (row >= n_s) return;
+  uint32_t lo = 0, hi = 0;
+  for (int64_t j = indptr[row] + lane; j < indptr[row + 1]; j += 32) {
+    const int32_t f = indices[j];
+    if (f >= 0 && f < d) {
+      const int32_t sl = head_slot[f];
+      if (sl >= 0) {
+        if (sl < 32) lo |= 1u << sl;
+        else hi |= 1u << (sl - 32);
+      }
+    }
+  }
+  lo = __reduce_or_sync(0xffffffffu, lo);
+  hi = __reduce_or_sync(0xffffffffu, hi);
+  if (lane == 0) cols[row] = ((uint64_t)hi << 32) | lo;
+}
+
 }  // namespace
+
+// minimum df of a head feature (0xFFFFFFFF = no heads); BINARY S only
+uint32_t head_min_df(const knnjoin_csr* S, const knnjoin_options* opt) {
+  if (S->dtype != KNNJOIN_BINARY || S->n_rows == 0) return 0xFFFFFFFFu;
+  float dens = opt ? opt->head_density : 0.0f;
+  if (dens < 0.0f) return 0xFFFFFFFFu;
+  if (dens == 0.0f) dens = kDefaultHeadDensity;
+  double m = ceil((double)dens * (double)S->n_rows);
+  if (m < 1.0) m = 1.0;
+  return m > 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)m;
+}
+
 }  // namespace kj
 
 using namespace kj;
@@ -252,7 +387,7 @@ KJ_API size_t knnjoin_build_workspace_bytes(const knnjoin_csr* S, int32_t d, con
   if (!check_build_args(S, d, opt, &tile)) return 0;
   IndexLayout L;
   BuildWs W;
-  if (!index_layout(S, d, tile, &L) || !build_ws_layout(S, L, &W)) { set_error("workspace sizing failed"); return 0; }
+  if (!index_layout(S, d, tile, &L) || !build_ws_layout(S, d, L, &W)) { set_error("workspace sizing failed"); return 0; }
   return W.total;
 }
 
@@ -273,7 +408,7 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   if (S->dtype == KNNJOIN_INT8 && S->nnz > 0 && !S->values) { set_error("INT8 S needs values"); return KNNJOIN_ERR_ARG; }
   IndexLayout L;
   BuildWs W;
-  if (!index_layout(S, d, tile, &L) || !build_ws_layout(S, L, &W)) { set_error("layout failed"); return KNNJOIN_ERR_ARG; }
+  if (!index_layout(S, d, tile, &L) || !build_ws_layout(S, d, L, &W)) { set_error("layout failed"); return KNNJOIN_ERR_ARG; }
   if (!storage || storage_bytes < L.total) { set_error("index storage %zu < %zu bytes", storage_bytes, L.total); return KNNJOIN_ERR_WORKSPACE; }
   if (!workspace || workspace_bytes < W.total) { set_error("build workspace %zu < %zu bytes", workspace_bytes, W.total); return KNNJOIN_ERR_WORKSPACE; }
   if (((uintptr_t)storage & 255) || ((uintptr_t)workspace & 255)) { set_error("storage and workspace must be 256-byte aligned"); return KNNJOIN_ERR_ARG; }
@@ -283,6 +418,9 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   char* wb = (char*)workspace;
   uint32_t* off = (uint32_t*)(sb + L.off_at);
   int32_t* df = (int32_t*)(sb + L.df_at);
+  int32_t* head_slot = (int32_t*)(sb + L.head_slot_at);
+  int32_t* head_feat = (int32_t*)(sb + L.head_feat_at);
+  uint64_t* head_cols = (uint64_t*)(sb + L.head_cols_at);
   uint16_t* ids = (uint16_t*)(sb + L.ids_at);
   uint8_t* vals = S->dtype == KNNJOIN_INT8 ? (uint8_t*)(sb + L.vals_at) : nullptr;
   uint32_t* counts = (uint32_t*)(wb + W.counts_at);
@@ -292,13 +430,20 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   uint32_t* kb = (uint32_t*)(wb + W.kb_at);
   uint32_t* va = (uint32_t*)(wb + W.va_at);
   uint32_t* vb = (uint32_t*)(wb + W.vb_at);
+  uint32_t* dfk = (uint32_t*)(wb + W.dfk_at);
+  uint32_t* dfk2 = (uint32_t*)(wb + W.dfk2_at);
+  int32_t* fv = (int32_t*)(wb + W.fv_at);
+  int32_t* fv2 = (int32_t*)(wb + W.fv2_at);
   void* cubtmp = wb + W.cub_at;
-  uint32_t sentinel_key = (uint32_t)(L.n_off - 1);
-  const uint32_t dense_min = dense_threshold(S, tile, opt);
-  const uint32_t dense_units = (uint32_t)tile / 128u;
+  const uint32_t sentinel_key = (uint32_t)(L.n_off - 1);
+  const uint32_t min_df = head_min_df(S, opt);
+  int32_t head_max = (opt && opt->head_max > 0) ? opt->head_max : kMaxHead;
+  if (min_df == 0xFFFFFFFFu) head_max = 0;
 
   cudaError_t e;
   if ((e = cudaMemsetAsync(counts, 0, 4 * (size_t)L.n_off, st)) != cudaSuccess) return cuda_fail(e, "memset counts");
+  if ((e = cudaMemsetAsync(head_slot, 0xFF, 4 * (size_t)d, st)) != cudaSuccess) return cuda_fail(e, "memset head_slot");
+  if ((e = cudaMemsetAsync(head_cols, 0, 8 * (size_t)L.n_tiles * tile, st)) != cudaSuccess) return cuda_fail(e, "memset head_cols");
   if (vals && (e = cudaMemsetAsync(vals, 0, 8 * (size_t)L.unit_cap, st)) != cudaSuccess) return cuda_fail(e, "memset vals");
   const unsigned gnnz = (unsigned)((S->nnz + 255) / 256);
   if (S->nnz > 0) {
@@ -313,8 +458,15 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
     k_seg_count<<<gnnz, 256, 0, st>>>(kb, S->nnz, sentinel_key, first, counts);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_seg");
   }
-  k_df<<<(unsigned)(((int64_t)d * 32 + 255) / 256), 256, 0, st>>>(counts, d, L.n_tiles, df);
-  k_units<<<(unsigned)((L.n_off + 255) / 256), 256, 0, st>>>(counts, units, L.n_off, dense_min, dense_units);
+  k_df<<<(unsigned)(((int64_t)d * 32 + 255) / 256), 256, 0, st>>>(counts, d, L.n_tiles, df, dfk, fv);
+  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_df");
+  {
+    size_t tb = W.cub_bytes;
+    if ((e = cub::DeviceRadixSort::SortPairsDescending(cubtmp, tb, dfk, dfk2, fv, fv2, d, 0, 32, st)) != cudaSuccess)
+      return cuda_fail(e, "df sort");
+  }
+  k_head_select<<<1, 32, 0, st>>>(dfk2, fv2, d, min_df, head_max, head_slot, head_feat);
+  k_units<<<(unsigned)((L.n_off + 255) / 256), 256, 0, st>>>(counts, units, L.n_off, L.n_tiles, head_slot);
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_units");
   {
     size_t tb = W.cub_bytes;
@@ -323,16 +475,21 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   k_fill_pads<<<(unsigned)((L.unit_cap + 255) / 256), 256, 0, st>>>((uint4*)ids, L.unit_cap, (uint32_t)tile);
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_fill_pads");
   if (S->nnz > 0) {
-    if (dense_min != 0xFFFFFFFFu) {
-      k_zero_dense<<<(unsigned)((L.n_off - 1 + 255) / 256), 256, 0, st>>>(counts, off, L.n_off - 1, dense_min,
-                                                                        dense_units, (uint4*)ids);
-      if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_zero_dense");
-    }
-    k_scatter<<<gnnz, 256, 0, st>>>(kb, vb, S->nnz, off, first, counts, dense_min, sentinel_key, ids, vals);
+    k_scatter<<<gnnz, 256, 0, st>>>(kb, vb, S->nnz, off, first, units, sentinel_key, ids, vals);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_scatter");
-    if (dense_min != 0xFFFFFFFFu) {
-      k_mark_dense<<<(unsigned)((L.n_off - 1 + 255) / 256), 256, 0, st>>>(counts, off, L.n_off - 1, dense_min);
-      if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_mark_dense");
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t want = (L.n_off - 1 + 7) / 8;
+    const int64_t cap = (int64_t)sms * 16;
+    const unsigned grid = (unsigned)(want < cap ? (want > 0 ? want : 1) : cap);
+    k_block_layout<<<grid, 256, 0, st>>>(off, units, L.n_off - 1, (uint32_t)tile, ids, vals);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_block_layout");
+    if (head_max > 0) {
+      int64_t threads = S->n_rows * 32;
+      k_head_cols<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(S->indptr, S->indices, S->n_rows, d, head_slot,
+                                                                   head_cols);
+      if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_head_cols");
     }
   }
   knnjoin_index* h = new (std::nothrow) knnjoin_index();
@@ -345,9 +502,13 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   h->n_off = L.n_off;
   h->unit_cap = L.unit_cap;
   h->s_dtype = S->dtype;
-  h->dense_min = dense_min == 0xFFFFFFFFu ? 0x7FFFFFFF : (int32_t)dense_min;
+  h->head_min_df = min_df;
+  h->head_max = head_max;
   h->off = off;
   h->df = df;
+  h->head_slot = head_slot;
+  h->head_feat = head_feat;
+  h->head_cols = head_cols;
   h->ids = ids;
   h->vals = vals;
   h->storage_bytes = L.total;
@@ -366,7 +527,8 @@ KJ_API knnjoin_status knnjoin_index_stats(const knnjoin_index* idx, knnjoin_inde
   out->unit_capacity = idx->unit_cap;
   out->storage_bytes = (int64_t)idx->storage_bytes;
   out->s_dtype = idx->s_dtype;
-  out->dense_min = idx->dense_min;
+  out->head_min_df = idx->head_min_df == 0xFFFFFFFFu ? -1 : (int64_t)idx->head_min_df;
+  out->head_max = idx->head_max;
   return KNNJOIN_OK;
 }
 

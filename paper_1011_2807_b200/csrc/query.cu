@@ -34,6 +34,9 @@ struct QP {
   const uint32_t* off;
   const uint16_t* ids;
   const uint8_t* vals;
+  const int32_t* head_slot;  // [d] head slot or -1
+  const int32_t* head_feat;  // [kMaxHead + 1]; [kMaxHead] = number of head features
+  const uint64_t* head_cols; // [n_tiles * T] head-feature bits per S row
   int32_t d, T;
   int64_t NT;
   int64_t s_id_base;
@@ -182,12 +185,20 @@ __host__ __device__ inline size_t acc_region_bytes(int B, int T, int k, int NW) 
 }
 
 // shared-memory layout of k_accumulate_topk<B, ., ., NW>; the kernel derives its pointers from the same sums.
-// Staging: q[kCap][QS] (QS = 4 or 8: 16-byte rows), ustart[kCap], fm[kCap], P[kCap + 1].
-__host__ __device__ constexpr int q_stride(int B) { return B <= 4 ? 4 : 8; }
+// Staging of one chunk of runs: q[cap][B], ustart[cap], fm[cap], P[cap + 1]; cap = runs per chunk (384 for
+// 8-warp CTAs so that two CTAs with B = 3 fit on one SM, 512 for 16-warp CTAs).
+__host__ __device__ constexpr int kcap(int NW) { return NW == 8 ? 384 : 512; }
 __host__ __device__ inline size_t staging_at(int B, int T, int k, int NW) { return acc_region_bytes(B, T, k, NW); }
+// Head tables: lut[16 groups][B][16] u32 (entry m of group g, row b = sum of q over the set bits of m among
+// head slots 4g..4g+3) and head_mask[B] u64 (head slots present in row b).  The per-slot q values they are
+// built from (q_head[kMaxHead][B]) alias the staging area, which is free during batch setup.
+__host__ __device__ inline size_t head_at(int B, int T, int k, int NW) {
+  return align_up(staging_at(B, T, k, NW) + (size_t)kcap(NW) * B * 4 + (size_t)kcap(NW) * 8 +
+                      (size_t)(kcap(NW) + 1) * 4, 16);
+}
+__host__ __device__ inline size_t head_bytes(int B) { return (size_t)(kMaxHead / 4) * B * 16 * 4 + (size_t)B * 8; }
 __host__ __device__ inline size_t tail_at(int B, int T, int k, int NW) {
-  return align_up(staging_at(B, T, k, NW) + (size_t)kCap * q_stride(B) * 4 + (size_t)kCap * 8 +
-                      (size_t)(kCap + 1) * 4, 16);
+  return align_up(head_at(B, T, k, NW) + head_bytes(B), 16);
 }
 __host__ __device__ inline size_t smem_bytes(int B, int T, int k, int NW) {
   return tail_at(B, T, k, NW) + (size_t)NW * 8 /* scan partials */ + 8 * 8 /* theta_row */ + 32 /* misc */;
@@ -197,79 +208,30 @@ __device__ __forceinline__ void red_add_shared(uint32_t addr, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
-// Adds the dense (bitmap) slices staged at [kCap - n_dense, kCap) to the 4 columns [seg0 + 4*lane, +4) of
-// every batch row: v[b][j] += q_b if bit(col) is set (q_b is 0 for rows without the feature, so no per-run
-// row mask is consulted).  seg0 is the first column of the warp's 128-column step.  Returns the number of
-// (posting, row) visits applied by this lane when counting is on.
-__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t d;
-  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  return d;
-}
-
-template <int B, bool COUNT>
-__device__ __forceinline__ unsigned long long dense_add(uint32_t (&v)[B][4], int seg0, int n_dense,
-                                                        const uint16_t* __restrict__ ids, const uint32_t* s_ustart,
-                                                        const uint32_t* s_fm, const int32_t* s_q, int lane) {
-  const uint32_t* words = (const uint32_t*)ids + (seg0 >> 5) + (lane >> 3);
-  const int sh = (lane & 7) * 4;
-  unsigned long long nv = 0;
-  constexpr int U = 4;
-  uint32_t w[U];
-  int e0 = kCap - n_dense;
-#pragma unroll
-  for (int u = 0; u < U; ++u) w[u] = (e0 + u < kCap) ? __ldg(words + (size_t)s_ustart[e0 + u] * 4) : 0u;
-  for (; e0 < kCap; e0 += U) {
-    uint32_t wn[U];  // next group's bitmap words, in flight while this group is applied
-#pragma unroll
-    for (int u = 0; u < U; ++u) wn[u] = (e0 + U + u < kCap) ? __ldg(words + (size_t)s_ustart[e0 + U + u] * 4) : 0u;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (e0 + u < kCap) {
-        const uint32_t nib = w[u] >> sh;
-        const uint32_t b0 = nib & 1u, b1 = (nib >> 1) & 1u, b2 = (nib >> 2) & 1u, b3 = (nib >> 3) & 1u;
-        int32_t q[q_stride(B)];
-#pragma unroll
-        for (int h = 0; h < q_stride(B) / 4; ++h) {
-          const int4 q4 = *(const int4*)(s_q + (e0 + u) * q_stride(B) + 4 * h);
-          q[4 * h] = q4.x; q[4 * h + 1] = q4.y; q[4 * h + 2] = q4.z; q[4 * h + 3] = q4.w;
-        }
-#pragma unroll
-        for (int b = 0; b < B; ++b) {
-          const uint32_t qb = (uint32_t)q[b];
-          v[b][0] = mad_u32(b0, qb, v[b][0]);
-          v[b][1] = mad_u32(b1, qb, v[b][1]);
-          v[b][2] = mad_u32(b2, qb, v[b][2]);
-          v[b][3] = mad_u32(b3, qb, v[b][3]);
-        }
-        if (COUNT) nv += (unsigned long long)__popc(nib & 0xFu) * __popc(s_fm[e0 + u] >> 24);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) w[u] = wn[u];
-  }
-  return nv;
-}
-
 constexpr int kWinChunk = 8;  // 32-unit windows a warp takes per grab of the dynamic window counter
 
 template <int B, int KS, bool SINT8, int NW>
 __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
   constexpr int NT_ = NW * 32;        // threads per CTA
-  constexpr int IPT = kCap / NT_;     // staged runs per thread
+  constexpr int kCap = kcap(NW);      // runs staged per chunk
+  constexpr int IPT = (kCap + NT_ - 1) / NT_;  // staged runs per thread (the last may be partial)
   extern __shared__ __align__(16) unsigned char smem[];
   const int T = p.T;
   const int TS = acc_stride(T);
   uint32_t* acc = (uint32_t*)smem;
   const uint32_t acc_s = (uint32_t)__cvta_generic_to_shared(acc);
-  constexpr int QS = q_stride(B);
+  constexpr int QS = B;
   int32_t* s_q = (int32_t*)(smem + staging_at(B, T, p.k, NW));
   uint32_t* s_ustart = (uint32_t*)(s_q + kCap * QS);
   uint32_t* s_fm = s_ustart + kCap;
   uint32_t* s_P = s_fm + kCap;
+  uint32_t* s_lut = (uint32_t*)(smem + head_at(B, T, p.k, NW));  // [16][B][16]
+  uint64_t* s_hmask = (uint64_t*)(s_lut + (kMaxHead / 4) * B * 16);  // [B]
+  int32_t* s_qh = s_q;                                                // [kMaxHead][B], aliases staging
+  static_assert(kMaxHead * B <= kcap(NW) * B, "q_head must fit in the staging area");
   uint64_t* s_warp = (uint64_t*)(smem + tail_at(B, T, p.k, NW));
   uint64_t* s_theta = s_warp + NW;
-  int* s_misc = (int*)(s_theta + 8);  // [0] batch, [1] n sparse items, [2] TOT, [3] window counter, [4] n dense
+  int* s_misc = (int*)(s_theta + 8);  // [0] batch, [1] n sparse items, [2] TOT, [3] window counter
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = p.k;
@@ -285,6 +247,8 @@ __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
     }
   };
   unsigned long long n_visits = 0, n_inserts = 0;
+  const int n_head = p.head_feat[kMaxHead];
+  const int n_groups = (n_head + 3) >> 2;
 
   for (int i = tid; i < (int)(acc_region_bytes(B, T, k, NW) / 16); i += NT_) ((uint4*)acc)[i] = make_uint4(0, 0, 0, 0);
 
@@ -308,6 +272,33 @@ __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
 #pragma unroll
       for (int s = 0; s < KS; ++s) L[b][s] = 0;
     }
+    // ------------------------------------------------------------------ head tables of this batch
+    if (n_groups) {
+      for (int i = tid; i < kMaxHead * B; i += NT_) s_qh[i] = 0;
+      if (tid < B) s_hmask[tid] = 0;
+      __syncthreads();
+      for (int i = tid; i < nruns; i += NT_) {
+        const size_t run = (size_t)(run_base + i);
+        const uint32_t fm = p.runs_f[run];
+        const int sl = p.head_slot[fm & 0xFFFFFFu];
+        if (sl >= 0) {
+#pragma unroll
+          for (int b = 0; b < B; ++b) s_qh[sl * B + b] = p.runs_q[run * B + b];
+#pragma unroll
+          for (int b = 0; b < B; ++b)
+            if (fm & (1u << (24 + b))) atomicOr((unsigned long long*)&s_hmask[b], 1ull << sl);
+        }
+      }
+      __syncthreads();
+      for (int i = tid; i < n_groups * B * 16; i += NT_) {
+        const int g = i / (B * 16), b = (i / 16) % B, m = i & 15;
+        uint32_t v = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (m & (1 << j)) v += (uint32_t)s_qh[(4 * g + j) * B + b];
+        s_lut[i] = v;
+      }
+    }
     __syncthreads();
     phase_mark(5);
 
@@ -315,50 +306,45 @@ __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
     for (int64_t t = 0; t < ntiles; ++t) {
       for (int c0 = 0; c0 < nruns; c0 += kCap) {
         // ---------------------------------------------------------------- stage chunk of runs
-        // sparse (id-list) slices are compacted to the front with their position P in the flattened unit
-        // stream; dense (bitmap) slices are compacted to the back, [kCap - n_dense, kCap)
+        // non-empty slices are compacted with their position P in the flattened unit stream (head
+        // features have empty slices: their postings live in head_cols)
         {
           uint32_t fm[IPT], u0[IPT], U[IPT];
           uint64_t pk[IPT], mine = 0;
 #pragma unroll
           for (int it = 0; it < IPT; ++it) {
-            const int i = c0 + tid * IPT + it;
+            const int li = tid + it * NT_;  // run li of this chunk
+            const int i = c0 + li;
             fm[it] = 0; u0[it] = 0; U[it] = 0;
-            bool dense = false;
-            if (i < nruns) {
+            if (li < kCap && i < nruns) {
               fm[it] = p.runs_f[(size_t)(run_base + i)];
               const uint32_t* o = p.off + (size_t)(fm[it] & 0xFFFFFFu) * (size_t)(p.NT + 1) + (size_t)t;
-              const uint32_t a0 = o[0], a1 = o[1];
-              dense = (a0 & kDenseFlag) != 0;
-              u0[it] = a0 & kOffMask;
-              U[it] = (a1 & kOffMask) - u0[it];
+              u0[it] = o[0];
+              U[it] = o[1] - u0[it];
             }
-            const bool sp = !dense && U[it] > 0;
-            pk[it] = ((uint64_t)dense << 48) | ((uint64_t)sp << 32) | (sp ? U[it] : 0u);
+            pk[it] = ((uint64_t)(U[it] > 0) << 32) | U[it];
             mine += pk[it];
           }
           uint64_t total;
           uint64_t ex = block_exclusive_scan_u64<NW>(mine, s_warp, &total);
 #pragma unroll
           for (int it = 0; it < IPT; ++it) {
-            const bool dense = (pk[it] >> 48) != 0, sp = ((pk[it] >> 32) & 0xFFFFu) != 0;
-            if (sp || dense) {
-              const uint32_t c = sp ? (uint32_t)((ex >> 32) & 0xFFFFu) : (uint32_t)(kCap - 1 - (int)(ex >> 48));
+            if (U[it] > 0) {
+              const uint32_t c = (uint32_t)(ex >> 32);
               s_ustart[c] = u0[it];
-              if (sp) s_P[c] = (uint32_t)ex;
+              s_P[c] = (uint32_t)ex;
               s_fm[c] = fm[it];
-              const size_t run = (size_t)(run_base + c0 + tid * IPT + it);
+              const size_t run = (size_t)(run_base + c0 + tid + it * NT_);
 #pragma unroll
               for (int b = 0; b < B; ++b) s_q[c * QS + b] = p.runs_q[run * B + b];
             }
             ex += pk[it];
           }
           if (tid == 0) {
-            const uint32_t ns = (uint32_t)((total >> 32) & 0xFFFFu);
+            const uint32_t ns = (uint32_t)(total >> 32);
             s_misc[1] = (int)ns;
             s_misc[2] = (int)(uint32_t)total;
             s_misc[3] = 0;
-            s_misc[4] = (int)(total >> 48);
             s_P[ns] = (uint32_t)total;
           }
           __syncthreads();
@@ -458,36 +444,21 @@ __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
           __syncthreads();
           phase_mark(1);
         }
-        // ---------------------------------------------------------------- dense slices of a non-final chunk
-        if (c0 + kCap < nruns && s_misc[4] > 0) {
-          const int n_dense = s_misc[4];
-          const int cols = T / NW;
-          for (int c = 0; c < cols; c += 128) {
-            const int col = warp * cols + c + lane * 4;
-            uint32_t v[B][4];
-#pragma unroll
-            for (int b = 0; b < B; ++b) {
-              const uint4 x = *(const uint4*)(acc + (size_t)b * TS + col);
-              v[b][0] = x.x; v[b][1] = x.y; v[b][2] = x.z; v[b][3] = x.w;
-            }
-            if (p.counters) n_visits += dense_add<B, true>(v, warp * cols + c, n_dense, p.ids, s_ustart, s_fm, s_q, lane);
-            else dense_add<B, false>(v, warp * cols + c, n_dense, p.ids, s_ustart, s_fm, s_q, lane);
-#pragma unroll
-            for (int b = 0; b < B; ++b) *(uint4*)(acc + (size_t)b * TS + col) = make_uint4(v[b][0], v[b][1], v[b][2], v[b][3]);
-          }
-          __syncthreads();
-          phase_mark(2);
-        }
       }
       // -------------------------------------------------------------------- scan + top-k (a5)
       // warp w owns columns [w*T/NW, (w+1)*T/NW); per 128-column step every lane reads 4 scores of each row,
-      // adds the dense (bitmap) slices of the last staged chunk in registers, zero-fills, and offers keys
-      // above theta to the warp's register top-k list of that row.
+      // adds the head features from the batch's lookup tables (one table read per 4 head features per
+      // row and column), zero-fills, and offers keys above theta to the warp's register top-k list.
       {
         const int cols = T / NW;
         const int cbase = warp * cols;
         const uint32_t gbase = (uint32_t)(p.s_id_base + t * (int64_t)T);
-        const int n_dense = s_misc[4];
+        const uint64_t* hcols = p.head_cols + (size_t)t * T + cbase + lane * 4;
+        ulonglong2 hA = make_ulonglong2(0, 0), hB = make_ulonglong2(0, 0);
+        if (n_groups) {
+          hA = __ldg((const ulonglong2*)hcols);
+          hB = __ldg((const ulonglong2*)(hcols + 2));
+        }
         uint64_t th[B];
 #pragma unroll
         for (int b = 0; b < B; ++b) {
@@ -508,9 +479,29 @@ __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
               v[b][0] = v[b][1] = v[b][2] = v[b][3] = 0;
             }
           }
-          if (n_dense) {
-            if (p.counters) n_visits += dense_add<B, true>(v, cbase + c, n_dense, p.ids, s_ustart, s_fm, s_q, lane);
-            else dense_add<B, false>(v, cbase + c, n_dense, p.ids, s_ustart, s_fm, s_q, lane);
+          if (n_groups) {
+            const uint64_t hw[4] = {hA.x, hA.y, hB.x, hB.y};
+            if (c + 128 < cols) {  // next step's head words in flight while this step's tables are read
+              hA = __ldg((const ulonglong2*)(hcols + c + 128));
+              hB = __ldg((const ulonglong2*)(hcols + c + 130));
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint32_t lo = (uint32_t)hw[j], hi = (uint32_t)(hw[j] >> 32);
+#pragma unroll
+              for (int g = 0; g < kMaxHead / 4; ++g) {
+                if (g < n_groups) {
+                  const uint32_t m = ((g < 8 ? lo : hi) >> (4 * (g & 7))) & 15u;
+                  const uint32_t* lut = s_lut + g * B * 16 + m;
+#pragma unroll
+                  for (int b = 0; b < B; ++b) v[b][j] += lut[b * 16];
+                }
+              }
+              if (p.counters) {
+#pragma unroll
+                for (int b = 0; b < B; ++b) n_visits += __popcll(hw[j] & s_hmask[b]);
+              }
+            }
           }
           const uint32_t g0 = gbase + (uint32_t)col;
 #pragma unroll
@@ -795,6 +786,9 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
   p.off = idx->off;
   p.ids = idx->ids;
   p.vals = idx->vals;
+  p.head_slot = idx->head_slot;
+  p.head_feat = idx->head_feat;
+  p.head_cols = idx->head_cols;
   p.d = idx->d;
   p.T = idx->tile;
   p.NT = idx->n_tiles;

@@ -35,13 +35,18 @@ def test_index_bytes_host_only():
     import paper_1011_2807_b200._binding as b
     L = b._lib
     S = b._CSR(100_000, 4_000_000, 0, 0, 0, b.BINARY)
-    opt = b._Options(8192, 0, 0.0, 0)
+    opt = b._Options(8192, 0, 0.0, 0.0, 0)
     n = L.knnjoin_index_bytes(ctypes.byref(S), 10_000, ctypes.byref(opt))
     nt = (100_000 + 8191) // 8192
     n_off = 10_000 * (nt + 1) + 1
     cap = 4_000_000 // 8 + min(4_000_000, 10_000 * nt) + 1
     al = lambda x: (x + 255) // 256 * 256
-    assert n == al(al(al(4 * n_off) + 4 * 10_000) + 16 * cap)
+    at = al(4 * n_off)          # off
+    at = al(at + 4 * 10_000)    # df
+    at = al(at + 4 * 10_000)    # head_slot
+    at = al(at + 4 * 65)        # head_feat + n_head
+    at = al(at + 8 * nt * 8192)  # head_cols
+    assert n == al(at + 16 * cap)
 
 
 @pytest.mark.parametrize("d,tile,dtype,msg", [(0, 8192, 0, "d must be"), (100, 1000, 0, "tile"), (100, 8192, 2, "dtype")])
@@ -49,6 +54,6 @@ def test_build_argument_errors(d, tile, dtype, msg):
     import paper_1011_2807_b200._binding as b
     L = b._lib
     S = b._CSR(10, 20, 0, 0, 0, dtype)
-    opt = b._Options(tile, 0, 0.0, 0)
+    opt = b._Options(tile, 0, 0.0, 0.0, 0)
     assert L.knnjoin_index_bytes(ctypes.byref(S), d, ctypes.byref(opt)) == 0
     assert msg in b.knnjoin_last_error()

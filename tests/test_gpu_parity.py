@@ -146,80 +146,99 @@ def test_validate_csr():
     assert kj.knnjoin_validate_csr(oob, 8) == (3, 1)
 
 
-@pytest.mark.parametrize("name,T", [("C5", 4096), ("C2", 2048), ("C2", 8192)])
-def test_index_layout_matches_scipy_csc(name, T):
-    """T3: decode the built index (id-list and bitmap slices per (feature, tile)) and compare with scipy's CSC
-    restricted to each tile; df exact."""
+@pytest.mark.parametrize("name,T,hd", [("C5", 4096, 0.0), ("C2", 2048, 0.0), ("C2", 8192, 0.05)])
+def test_index_layout_matches_scipy_csc(name, T, hd):
+    """T3: decode the built index (id-list slices per (feature, tile) + head-feature words) and compare with
+    scipy's CSC restricted to each tile; df exact; head features are the most frequent ones."""
     import scipy.sparse as sp
     import paper_1011_2807_b200 as kj
     c = gen.CONFIGS[name].scaled(10, 9000)
     S = gen.generate(c, "S")
     dS = kj.DeviceCSR.from_host(S)
-    idx = kj.knnjoin_build_index(dS, c.d, tile=T)
+    idx = kj.knnjoin_build_index(dS, c.d, tile=T, head_density=hd)
     torch.cuda.synchronize()
     st = kj.knnjoin_index_stats(idx)
     raw = idx.storage.cpu().numpy()
     NT = st["n_tiles"]
     n_off = st["offsets"]
-    off_raw = raw[:4 * n_off].view(np.uint32)
-    dense_flag = (off_raw >> 31).astype(bool)
-    off = off_raw & 0x7FFFFFFF
+    off = raw[:4 * n_off].view(np.uint32)
     al = lambda x: (x + 255) // 256 * 256
     df_at = al(4 * n_off)
     df = raw[df_at:df_at + 4 * c.d].view(np.int32)
-    ids_at = al(df_at + 4 * c.d)
+    hs_at = al(df_at + 4 * c.d)
+    head_slot = raw[hs_at:hs_at + 4 * c.d].view(np.int32)
+    hf_at = al(hs_at + 4 * c.d)
+    head_feat = raw[hf_at:hf_at + 4 * 65].view(np.int32)
+    hc_at = al(hf_at + 4 * 65)
+    head_cols = raw[hc_at:hc_at + 8 * NT * T].view(np.uint64)
+    ids_at = al(hc_at + 8 * NT * T)
     cap = st["unit_capacity"]
     ids = raw[ids_at:ids_at + 16 * cap].view(np.uint16)
-    words = raw[ids_at:ids_at + 16 * cap].view(np.uint32)
     vals = None
     if S.values is not None:
         vals_at = al(ids_at + 16 * cap)
         vals = raw[vals_at:vals_at + 8 * cap].view(np.uint8)
-    np.testing.assert_array_equal(df, np.bincount(S.indices, minlength=c.d))
+    want_df = np.bincount(S.indices, minlength=c.d)
+    np.testing.assert_array_equal(df, want_df)
+    n_head = int(head_feat[64])
+    heads = head_feat[:n_head]
+    if name == "C5":
+        assert n_head == 0
+    else:
+        assert n_head > 0
+        order = np.lexsort((np.arange(c.d), -want_df))  # df desc, feature asc
+        np.testing.assert_array_equal(heads, order[:n_head])
+        assert want_df[heads].min() >= int(np.ceil(st["head_min_df"]))
+        for i, f in enumerate(heads):
+            assert head_slot[f] == i
     data = np.ones(S.nnz, np.int64) if S.values is None else S.values.astype(np.int64)
     M = sp.csr_matrix((data, S.indices, S.indptr), shape=(S.n_rows, c.d)).tocsc()
-    n_dense = 0
-    for f in range(c.d):
+    # head words: bit i of head_cols[s] <=> s has heads[i]
+    for i, f in enumerate(heads):
+        bits = ((head_cols[:S.n_rows] >> np.uint64(i)) & np.uint64(1)).astype(bool)
+        want = np.zeros(S.n_rows, bool)
+        want[M[:, f].indices] = True
+        np.testing.assert_array_equal(bits, want)
+    assert not head_cols[S.n_rows:].any()
+    rng = np.random.default_rng(0)
+    for f in rng.choice(c.d, 400, replace=False):
         col = M[:, f]
         rows_f, vals_f = col.indices, col.data
         for t in range(NT):
             key = f * (NT + 1) + t
             a, b = int(off[key]), int(off[key + 1])
             sel = (rows_f >= t * T) & (rows_f < (t + 1) * T)
-            want = rows_f[sel] - t * T
-            if dense_flag[key]:
-                n_dense += 1
-                assert st["dense_min"] <= sel.sum() and b - a == T // 128
-                bits = np.unpackbits(words[4 * a:4 * b].view(np.uint8), bitorder="little")
-                np.testing.assert_array_equal(np.nonzero(bits)[0], want)
+            if head_slot[f] >= 0:
+                assert b == a
                 continue
             got = ids[8 * a:8 * b]
             keep = got < T
             assert np.all(got[~keep] < T + 32)
             order = np.argsort(got[keep])
-            np.testing.assert_array_equal(got[keep][order].astype(np.int64), want)
+            np.testing.assert_array_equal(got[keep][order].astype(np.int64), rows_f[sel] - t * T)
             if vals is not None:
                 np.testing.assert_array_equal(vals[8 * a:8 * b][keep][order], vals_f[sel])
             assert b - a == (sel.sum() + 7) // 8
-    if name == "C2":
-        assert n_dense > 0
-    else:
-        assert n_dense == 0
 
 
-@pytest.mark.parametrize("dense_min", [-1, 0, 1, 300])
-def test_dense_bitmap_modes(dense_min):
-    """Bitmap (dense) and id-list slices give identical results; dense_min=1 forces tile/16."""
+@pytest.mark.parametrize("hd,hm", [(-1.0, 0), (0.0, 0), (0.01, 0), (0.01, 5), (0.3, 0)])
+def test_head_feature_modes(hd, hm):
+    """Head features (lookup-table path) and id lists give identical results for any head set."""
     c = gen.CONFIGS["C2"].scaled(300, 30000)
     R, S = gen.generate(c, "R"), gen.generate(c, "S")
-    ids, sc = _check(R, S, c.k, tile=4096, dense_min=dense_min)
-    ref = gpu_join(R, S, c.k, tile=4096, dense_min=-1)
+    cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+    ids, sc = _check(R, S, c.k, tile=4096, head_density=hd, head_max=hm, counters=cnt)
+    ref = gpu_join(R, S, c.k, tile=4096, head_density=-1.0)
     np.testing.assert_array_equal(ids, ref[0])
     np.testing.assert_array_equal(sc, ref[1])
+    nR = np.bincount(R.indices, minlength=c.d)
+    nS = np.bincount(S.indices, minlength=c.d)
+    assert int(cnt[0]) == int((nR.astype(np.int64) * nS).sum())
 
 
-def test_dense_multi_chunk():
-    """More than 512 runs per batch (several staging chunks) with dense slices in non-final chunks."""
+@pytest.mark.parametrize("cta_warps,batch_rows", [(8, 3), (16, 6), (8, 1)])
+def test_multi_chunk_batches(cta_warps, batch_rows):
+    """More runs per batch than one staging chunk holds, with head features present."""
     rng = np.random.default_rng(7)
     d = 2000
     rows = []
@@ -229,7 +248,6 @@ def test_dense_multi_chunk():
         rows.append([(f, float(np.float32(rng.lognormal()))) for f in head + tail])
     R = csr_from_rows(rows, d, "fp32")
     S = random_csr(rng, 6000, d, 5, 40, "binary")
-    # make the head features dense in S
     Srows = []
     for i in range(S.n_rows):
         idx, _ = S.row(i)
@@ -237,7 +255,7 @@ def test_dense_multi_chunk():
         Srows.append(sorted(set(idx.tolist()) | set(extra.tolist())))
     S = csr_from_rows(Srows, d, "binary")
     cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
-    _check(R, S, 10, tile=2048, batch_rows=4, counters=cnt)
+    _check(R, S, 10, tile=2048, batch_rows=batch_rows, cta_warps=cta_warps, counters=cnt)
     nR = np.bincount(R.indices, minlength=d)
     nS = np.bincount(S.indices, minlength=d)
     assert int(cnt[0]) == int((nR.astype(np.int64) * nS).sum())
