@@ -485,22 +485,20 @@ __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
               hA = __ldg((const ulonglong2*)(hcols + c + 128));
               hB = __ldg((const ulonglong2*)(hcols + c + 130));
             }
+            for (int g = 0; g < n_groups; ++g) {
+              const uint32_t* lutg = s_lut + g * B * 16;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const uint32_t lo = (uint32_t)hw[j], hi = (uint32_t)(hw[j] >> 32);
+              for (int j = 0; j < 4; ++j) {
+                const uint32_t m = (uint32_t)(hw[j] >> (4 * g)) & 15u;
 #pragma unroll
-              for (int g = 0; g < kMaxHead / 4; ++g) {
-                if (g < n_groups) {
-                  const uint32_t m = ((g < 8 ? lo : hi) >> (4 * (g & 7))) & 15u;
-                  const uint32_t* lut = s_lut + g * B * 16 + m;
-#pragma unroll
-                  for (int b = 0; b < B; ++b) v[b][j] += lut[b * 16];
-                }
+                for (int b = 0; b < B; ++b) v[b][j] += lutg[b * 16 + m];
               }
-              if (p.counters) {
+            }
+            if (p.counters) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
 #pragma unroll
                 for (int b = 0; b < B; ++b) n_visits += __popcll(hw[j] & s_hmask[b]);
-              }
             }
           }
           const uint32_t g0 = gbase + (uint32_t)col;
