@@ -201,7 +201,7 @@ __host__ __device__ inline size_t tail_at(int B, int T, int k, int NW) {
   return align_up(head_at(B, T, k, NW) + head_bytes(B), 16);
 }
 __host__ __device__ inline size_t smem_bytes(int B, int T, int k, int NW) {
-  return tail_at(B, T, k, NW) + (size_t)NW * 8 /* scan partials */ + 8 * 8 /* theta_row */ + 32 /* misc */;
+  return tail_at(B, T, k, NW) + (size_t)NW * 8 /* scan partials */ + (size_t)B * NW * 8 /* theta */ + 32 /* misc */;
 }
 
 __device__ __forceinline__ void red_add_shared(uint32_t addr, uint32_t v) {
@@ -230,8 +230,8 @@ __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
   int32_t* s_qh = s_q;                                                // [kMaxHead][B], aliases staging
   static_assert(kMaxHead * B <= kcap(NW) * B, "q_head must fit in the staging area");
   uint64_t* s_warp = (uint64_t*)(smem + tail_at(B, T, p.k, NW));
-  uint64_t* s_theta = s_warp + NW;
-  int* s_misc = (int*)(s_theta + 8);  // [0] batch, [1] n sparse items, [2] TOT, [3] window counter
+  uint64_t* s_theta = s_warp + NW;    // [B][NW]: k-th key of each warp's list per row (no atomics needed)
+  int* s_misc = (int*)(s_theta + B * NW);  // [0] batch, [1] n sparse items, [2] TOT, [3] window counter
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = p.k;
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
     const int nb = (int)min((int64_t)B, p.n_r - row0);
     const int64_t run_base = p.r_indptr[row0];
     const int nruns = (int)p.batch_nruns[batch];
-    if (tid < 8) s_theta[tid] = kKeyFloor;
+    if (tid < B * NW) s_theta[tid] = kKeyFloor;
 
     uint64_t L[B][KS];
     uint64_t own[B];
@@ -459,13 +459,18 @@ __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
           hA = __ldg((const ulonglong2*)hcols);
           hB = __ldg((const ulonglong2*)(hcols + 2));
         }
+        // theta of row b = max over the warps' k-th keys: k keys at least that large exist in one list, so
+        // any candidate key below it cannot be in the row's final top-k (reading c1 total order)
+        auto row_theta = [&](int b) {
+          const volatile uint64_t* tb = s_theta + b * NW;
+          uint64_t m = own[b];
+#pragma unroll
+          for (int w = 0; w < NW; ++w) m = max(m, (uint64_t)tb[w]);
+          return m;
+        };
         uint64_t th[B];
 #pragma unroll
-        for (int b = 0; b < B; ++b) {
-          th[b] = own[b];
-          const uint64_t sh = *(volatile uint64_t*)&s_theta[b];
-          if (sh > th[b]) th[b] = sh;
-        }
+        for (int b = 0; b < B; ++b) th[b] = row_theta(b);
         for (int c = 0; c < cols; c += 128) {
           const int col = cbase + c + lane * 4;
           uint32_t v[B][4];
@@ -505,16 +510,13 @@ __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
 #pragma unroll
           for (int b = 0; b < B; ++b) {
             if (b < nb) {
-              const uint32_t thh = (uint32_t)(th[b] >> 32), thl = (uint32_t)th[b];
-              bool any = false;
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                any |= v[b][j] > thh || (v[b][j] == thh && (0xFFFFFFFFu - (g0 + j)) > thl);
-              if (__any_sync(0xffffffffu, any)) {
-                {
-                  const uint64_t sh = *(volatile uint64_t*)&s_theta[b];
-                  if (sh > th[b]) th[b] = sh;
-                }
+              // cheap superset test: key > theta needs score >= theta's score (+1 when theta's id part admits
+              // no id); the exact 64-bit key comparison happens in list_offer_lanes
+              const uint32_t thh = (uint32_t)(th[b] >> 32);
+              const uint32_t t32 = thh + ((uint32_t)th[b] == 0xFFFFFFFFu ? 1u : 0u);
+              const bool any = (v[b][0] >= t32) | (v[b][1] >= t32) | (v[b][2] >= t32) | (v[b][3] >= t32);
+              if (__any_sync(0xffffffffu, any) && t32 != 0u) {
+                th[b] = row_theta(b);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                   const uint64_t key = v[b][j] ? make_key(v[b][j], g0 + j) : 0;
@@ -524,7 +526,7 @@ __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
                 const uint64_t nk = list_kth<KS>(L[b], k);
                 if (nk > own[b]) {
                   own[b] = nk;
-                  if (lane == 0) atomicMax((unsigned long long*)&s_theta[b], (unsigned long long)nk);
+                  if (lane == 0) s_theta[b * NW + warp] = nk;
                 }
               }
             }
