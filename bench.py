@@ -241,8 +241,10 @@ def bench_ours(args):
     dS = kj.DeviceCSR.from_host(S, dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    def step(dS_, dR_, kernel_events=None):
+    def step(dS_, dR_, kernel_events=None, build_event=None):
         idx = kj.knnjoin_build_index(dS_, d, s_id_base=s_base, tile=args.tile, head_density=args.head_density, head_max=args.head_max)
+        if build_event is not None:
+            build_event.record(stream)
         if world == 1:
             ids, sc, _ = kj.knnjoin_query(idx, dR_, k, batch_rows=args.batch_rows, events=kernel_events,
                                           cta_warps=args.cta_warps)
@@ -276,6 +278,14 @@ def bench_ours(args):
     kj.knnjoin_query(idx_p, dR, k, batch_rows=args.batch_rows, phase_cycles=phase, cta_warps=args.cta_warps)
     torch.cuda.synchronize()
     ph = phase.cpu().tolist()
+    cnt = torch.zeros(4, dtype=torch.int64, device=dev)
+    idx_c = kj.knnjoin_build_index(dS, d, s_id_base=s_base, tile=args.tile, head_density=args.head_density,
+                                   head_max=args.head_max)
+    kj.knnjoin_query(idx_c, dR, k, batch_rows=args.batch_rows, counters=cnt, cta_warps=args.cta_warps)
+    torch.cuda.synchronize()
+    counters = dict(zip(["postings_visited", "inserts", "head_postings_skipped", "head_completions"],
+                        cnt.cpu().tolist()))
+    del idx_c
     tot_ph = max(1, sum(ph[:6]))
     phase_share = {n: round(ph[i] / tot_ph, 4) for i, n in
                    enumerate(["staging", "sparse_atomics", "unused", "scan_topk", "merge_output", "batch_setup_head_tables"])}
@@ -286,6 +296,7 @@ def bench_ours(args):
         ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         kb = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         ke = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        bd = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         for ev in kb + ke:  # materialise the cudaEvent handles; the library re-records them around its kernel
             ev.record(stream)
         if world > 1:
@@ -297,7 +308,7 @@ def bench_ours(args):
         for i in range(args.steps):
             flush.fill_(i & 0xFF)  # > L2 (126 MB): evict the previous step's index and inputs
             starts[i].record(stream)
-            step(dS, dR, (kb[i], ke[i]))
+            step(dS, dR, (kb[i], ke[i]), bd[i])
             ends[i].record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -305,7 +316,11 @@ def bench_ours(args):
         clocks = sampler.stop()
         step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
         kern_ms = [s.elapsed_time(e) for s, e in zip(kb, ke)]
+        build_ms.clear()
+        build_ms.extend(s.elapsed_time(e) for s, e in zip(starts, bd))
         return step_ms, kern_ms, clocks
+
+    build_ms = []
 
     step_ms, kern_ms, clocks = timed_region()
     if any(r in BAD_REASONS for r in clocks.get("reasons", [])):
@@ -396,8 +411,10 @@ def bench_ours(args):
         "clocks": clocks,
         "gpu_launches": (launches_per_step * args.steps) if launches_per_step is not None else None,
         "breakdown": {"kernel_ms": kern_avg_max, "step_ms": ms_per_step,
+                      "build_index_ms": sum(build_ms) / len(build_ms),
+                      "query_prep_ms": ms_per_step - kern_avg_max - sum(build_ms) / len(build_ms),
                       "other_ms": ms_per_step - kern_avg_max, "launches_per_step": launches_per_step,
-                      "kernel_phase_share": phase_share},
+                      "kernel_phase_share": phase_share, "counters": counters},
     }
     if e2e is not None:
         out["e2e"] = e2e

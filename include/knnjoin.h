@@ -62,11 +62,13 @@ typedef struct {
 /* Build options.  tile: S ids per tile (the S-block of Alg. 1 mapped to a shared-memory score array);
  * 0 = default 8192; must be a multiple of 2048 and <= 32768.
  * prune / alpha: reserved for the threshold-pruned mode; must be 0 / 0.
- * head_density / head_max: "head features" (BINARY S only).  Up to head_max (0 = 64, at most 64) of the
+ * head_density / head_max: "head features" (BINARY S only).  Up to head_max (0 = 32, at most 32) of the
  *   most frequent features with df >= head_density * |S| (0 = default 1/8, negative = no head features) are
- *   not stored as id lists: each S row gets one 64-bit word of head-feature bits, and the query adds their
- *   contributions from per-batch lookup tables (4 features per 16-entry table) during the top-k scan instead
- *   of one shared-memory atomic per posting.  Same integer sums, different encoding of I_d. */
+ *   not stored as id lists: each S row gets one 32-bit word of head-feature bits.  During the top-k scan the
+ *   query bounds their contribution to a score by the sum of the row's largest head weights (popcount of
+ *   the shared head bits) and adds it exactly, from per-batch 16-entry lookup tables, only where that bound
+ *   can beat the running k-th score (the threshold refinement of IIIB, applied to the
+ *   head features).  Results are identical; only the work changes. */
 typedef struct {
   int32_t tile;
   int32_t prune;
@@ -80,8 +82,10 @@ typedef struct {
  *  cta_warps:  warps per CTA of the accumulation kernel, 8 or 16 (0 = auto: 8-warp CTAs, two per SM,
  *              with the largest batch whose score arrays fit; else one 16-warp CTA per SM).
  *  counters:   NULL, or a device int64_t[4] that the query ADDS into: [0] postings visited (Eq. 4 second
- *              term), [1] candidate inserts into the top-k lists, [2] postings skipped by
- *              pruning (0 in unpruned mode), [3] completions (0 in unpruned mode).
+ *              term; head postings are counted whether or not their completion is skipped),
+ *              [1] candidate inserts into the top-k lists, [2] head postings whose exact addition was skipped
+ *              because the score bound could not reach the running k-th score, [3] exact head completions
+ *              ((row, S row) pairs).
  *  ev_begin / ev_end: NULL, or cudaEvent_t (as void*) recorded on `stream` immediately before and after
  *              the score-accumulation + top-k kernel, so callers can time that kernel alone.
  *  phase_cycles: NULL, or a device int64_t[8] that the query ADDS SM clock cycles into, summed over CTAs
@@ -127,7 +131,7 @@ size_t knnjoin_build_workspace_bytes(const knnjoin_csr* S, int32_t d, const knnj
  * contiguous, 16-byte aligned slice of local ids (+ uint8 values for INT8 S), padded with dummy ids
  * tile + (0..31); inside each full 256-posting block postings are ordered by shared-memory bank, the last
  * partial block is transposed so a warp's lanes touch consecutive ids; head features (see head_density)
- * are stored as one 64-bit word per S row instead of id lists.
+ * are stored as one 32-bit word per S row instead of id lists.
  * s_id_base: global id of S row 0 (ids returned by queries are s_id_base + local row).
  * S may be freed after the call's work completes on `stream`; the storage must outlive every query.
  * S dtype must be BINARY or INT8 (FP32 S -> KNNJOIN_ERR_UNSUPPORTED).  *out receives a host handle

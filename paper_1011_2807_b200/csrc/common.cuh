@@ -19,7 +19,7 @@ constexpr int kMaxK = 256;
 constexpr int kDefaultTile = 8192;
 constexpr int kMaxTile = 32768;        // local ids < tile; padding ids are tile + (0..31) (dummy columns)
 constexpr int kTileQuantum = 2048;     // tile must split into kWarps column strips of 128-column chunks
-constexpr int kMaxHead = 64;                  // head features per index (one 64-bit word per S row)
+constexpr int kMaxHead = 32;                  // head features per index (one 32-bit word per S row)
 constexpr float kDefaultHeadDensity = 0.125f;  // df >= |S|/8 makes a feature a head candidate
 constexpr int kPadCols = 32;           // dummy score columns per row that absorb padding postings
 constexpr uint64_t kKeyFloor = 0x00000000FFFFFFFFull;  // score 0 with every id: admits nothing
@@ -60,7 +60,7 @@ struct knnjoin_index {
   const int32_t* df = nullptr;         // [d] |I_d| (document frequency of each feature in S)
   const int32_t* head_slot = nullptr;  // [d] head slot of a feature, -1 if not a head feature
   const int32_t* head_feat = nullptr;  // [kMaxHead + 1] feature of each head slot (-1 unused); [kMaxHead] = n_head
-  const uint64_t* head_cols = nullptr; // [n_tiles * tile] bit i: S row has head feature head_feat[i]
+  const uint32_t* head_cols = nullptr; // [n_tiles * tile] bit i: S row has head feature head_feat[i]
   const uint16_t* ids = nullptr;       // [unit_cap*8] local S ids (< tile); padding = tile + (u mod 32)
   const uint8_t* vals = nullptr;       // [unit_cap*8] INT8 S weights (nullptr for BINARY S)
   size_t storage_bytes = 0;

@@ -10,10 +10,11 @@
 //                                                            entries hold tile + (u mod 32), a dummy column
 //   vals[8*u .. 8*u+8)                                       INT8 S weights (same positions)
 //
-// Head features.  For BINARY S, the (up to 64) most frequent features with df >= head_density * |S| are
-// not stored as id lists at all: every S row s gets a 64-bit word head_cols[s] whose bit i says "s has
-// head feature head_feat[i]".  The query accumulates them from per-batch lookup tables (Four Russians,
-// 4 features per table) instead of one shared-memory atomic per posting.
+// Head features.  For BINARY S, the (up to 32) most frequent features with df >= head_density * |S| are
+// not stored as id lists at all: every S row s gets a 32-bit word head_cols[s] whose bit i says "s has
+// head feature head_feat[i]".  The query bounds their contribution by a popcount and adds it exactly from
+// per-batch lookup tables (4 features per table) only where the bound can beat the running k-th score
+// (DESIGN.md "Head features").
 //
 // Steps (all stream-ordered, integer, deterministic, no contended atomics -- Zipf head features put every
 // row of a tile on the same key, so a global-atomic histogram would serialise):
@@ -28,7 +29,7 @@
 //      (id mod 32), so slot j of the 32 units holds postings of ~32 distinct banks; the final partial block
 //      of m units is transposed (unit i holds sorted postings i, i+m, ..., i+7m) so the lanes of a warp hit
 //      consecutive ids
-//   7. k_head_cols: one 64-bit head word per S row.
+//   7. k_head_cols: one 32-bit head word per S row.
 // The paper counts this as Eq. 4's first term, sum |s_i| postings.
 #include <cub/cub.cuh>
 
@@ -59,7 +60,7 @@ bool index_layout(const knnjoin_csr* S, int32_t d, int32_t tile, IndexLayout* L)
   L->head_feat_at = at;
   at = align_up(at + sizeof(int32_t) * (kMaxHead + 1), 256);  // [kMaxHead] features + n_head
   L->head_cols_at = at;
-  at = align_up(at + sizeof(uint64_t) * (size_t)L->n_tiles * tile, 256);
+  at = align_up(at + sizeof(uint32_t) * (size_t)L->n_tiles * tile, 256);
   L->ids_at = at;
   at = align_up(at + 16 * (size_t)L->unit_cap, 256);
   L->vals_at = at;
@@ -337,24 +338,20 @@ __global__ void k_block_layout(const uint32_t* __restrict__ off, const uint32_t*
 // warp per S row: bit i of head_cols[row] <=> row has head feature head_feat[i]; tail columns of the last
 // tile stay 0 (memset)
 __global__ void k_head_cols(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices, int64_t n_s,
-                            int32_t d, const int32_t* __restrict__ head_slot, uint64_t* __restrict__ cols) {
+                            int32_t d, const int32_t* __restrict__ head_slot, uint32_t* __restrict__ cols) {
   int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (row >= n_s) return;
-  uint32_t lo = 0, hi = 0;
+  uint32_t w = 0;
   for (int64_t j = indptr[row] + lane; j < indptr[row + 1]; j += 32) {
     const int32_t f = indices[j];
     if (f >= 0 && f < d) {
       const int32_t sl = head_slot[f];
-      if (sl >= 0) {
-        if (sl < 32) lo |= 1u << sl;
-        else hi |= 1u << (sl - 32);
-      }
+      if (sl >= 0) w |= 1u << sl;
     }
   }
-  lo = __reduce_or_sync(0xffffffffu, lo);
-  hi = __reduce_or_sync(0xffffffffu, hi);
-  if (lane == 0) cols[row] = ((uint64_t)hi << 32) | lo;
+  w = __reduce_or_sync(0xffffffffu, w);
+  if (lane == 0) cols[row] = w;
 }
 
 }  // namespace
@@ -420,7 +417,7 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   int32_t* df = (int32_t*)(sb + L.df_at);
   int32_t* head_slot = (int32_t*)(sb + L.head_slot_at);
   int32_t* head_feat = (int32_t*)(sb + L.head_feat_at);
-  uint64_t* head_cols = (uint64_t*)(sb + L.head_cols_at);
+  uint32_t* head_cols = (uint32_t*)(sb + L.head_cols_at);
   uint16_t* ids = (uint16_t*)(sb + L.ids_at);
   uint8_t* vals = S->dtype == KNNJOIN_INT8 ? (uint8_t*)(sb + L.vals_at) : nullptr;
   uint32_t* counts = (uint32_t*)(wb + W.counts_at);
@@ -443,7 +440,7 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   cudaError_t e;
   if ((e = cudaMemsetAsync(counts, 0, 4 * (size_t)L.n_off, st)) != cudaSuccess) return cuda_fail(e, "memset counts");
   if ((e = cudaMemsetAsync(head_slot, 0xFF, 4 * (size_t)d, st)) != cudaSuccess) return cuda_fail(e, "memset head_slot");
-  if ((e = cudaMemsetAsync(head_cols, 0, 8 * (size_t)L.n_tiles * tile, st)) != cudaSuccess) return cuda_fail(e, "memset head_cols");
+  if ((e = cudaMemsetAsync(head_cols, 0, 4 * (size_t)L.n_tiles * tile, st)) != cudaSuccess) return cuda_fail(e, "memset head_cols");
   if (vals && (e = cudaMemsetAsync(vals, 0, 8 * (size_t)L.unit_cap, st)) != cudaSuccess) return cuda_fail(e, "memset vals");
   const unsigned gnnz = (unsigned)((S->nnz + 255) / 256);
   if (S->nnz > 0) {

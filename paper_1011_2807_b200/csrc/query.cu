@@ -23,6 +23,8 @@
 //                 candidates with key > theta go into the warp's register top-k list; theta_row (shared,
 //                 atomicMax of every warp's k-th key) tightens every warp's filter.
 //        merge the 16 per-warp lists of each row, finalize (ids, scores, keys).
+#include <cub/cub.cuh>
+
 #include "common.cuh"
 #include "topk.cuh"
 
@@ -36,7 +38,7 @@ struct QP {
   const uint8_t* vals;
   const int32_t* head_slot;  // [d] head slot or -1
   const int32_t* head_feat;  // [kMaxHead + 1]; [kMaxHead] = number of head features
-  const uint64_t* head_cols; // [n_tiles * T] head-feature bits per S row
+  const uint32_t* head_cols; // [n_tiles * T] head-feature bits per S row
   int32_t d, T;
   int64_t NT;
   int64_t s_id_base;
@@ -93,14 +95,22 @@ __global__ void k_row_scale_kernel(const int64_t* __restrict__ indptr, const int
   }
 }
 
-// one warp per batch of B rows
-__global__ void k_build_runs(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                             const void* __restrict__ values, knnjoin_dtype rdt, int64_t n_r, int32_t d, int B,
-                             int64_t n_batches, const double* __restrict__ sigma, uint32_t* __restrict__ runs_f,
-                             int32_t* __restrict__ runs_q, uint32_t* __restrict__ batch_nruns) {
-  int64_t batch = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  if (batch >= n_batches) return;
+__device__ __forceinline__ int32_t quantize(const void* __restrict__ values, knnjoin_dtype rdt, int64_t j, double sg) {
+  if (rdt == KNNJOIN_FP32) {
+    int32_t q = (int32_t)rint((double)((const float*)values)[j] * sg);
+    return q < 1 ? 1 : q;
+  }
+  if (rdt == KNNJOIN_INT8) return (int32_t)((const int8_t*)values)[j];
+  return 1;
+}
+
+// One warp merges the B rows of `batch` (lane b < B walks row b): one run per distinct feature, in ascending
+// feature order.  Fallback for batches with more entries than the block sort below holds.
+__device__ void warp_merge_runs(int64_t batch, int lane, const int64_t* __restrict__ indptr,
+                                const int32_t* __restrict__ indices, const void* __restrict__ values,
+                                knnjoin_dtype rdt, int64_t n_r, int32_t d, int B, const double* __restrict__ sigma,
+                                uint32_t* __restrict__ runs_f, int32_t* __restrict__ runs_q,
+                                uint32_t* __restrict__ batch_nruns) {
   int64_t row = batch * B + lane;
   bool mine = lane < B && row < n_r;
   int64_t ptr = 0, end = 0;
@@ -128,15 +138,7 @@ __global__ void k_build_runs(const int64_t* __restrict__ indptr, const int32_t* 
     if (lane < B) {
       int32_t q = 0;
       if (has) {
-        if (rdt == KNNJOIN_FP32) {
-          double v = (double)((const float*)values)[ptr] * sg;
-          q = (int32_t)rint(v);
-          if (q < 1) q = 1;
-        } else if (rdt == KNNJOIN_INT8) {
-          q = (int32_t)((const int8_t*)values)[ptr];
-        } else {
-          q = 1;
-        }
+        q = quantize(values, rdt, ptr, sg);
         ++ptr;
       }
       runs_q[run * B + lane] = q;
@@ -145,6 +147,107 @@ __global__ void k_build_runs(const int64_t* __restrict__ indptr, const int32_t* 
     ++nruns;
   }
   if (lane == 0) batch_nruns[batch] = nruns;
+}
+
+constexpr int kRunThreads = 128;  // block sort: kRunThreads x ITEMS (row, feature) entries per batch
+
+// One CTA per batch: the batch's (feature, row) entries are block-radix-sorted in shared memory, equal
+// features collapse into one run (row mask + per-row q), runs are written in ascending feature order.
+// Batches with more entries than the capacity fall back to warp_merge_runs.
+template <int kRunItems>
+__global__ void __launch_bounds__(kRunThreads) k_build_runs(const int64_t* __restrict__ indptr,
+                                                            const int32_t* __restrict__ indices,
+                                                            const void* __restrict__ values, knnjoin_dtype rdt,
+                                                            int64_t n_r, int32_t d, int B, int64_t n_batches,
+                                                            const double* __restrict__ sigma,
+                                                            uint32_t* __restrict__ runs_f, int32_t* __restrict__ runs_q,
+                                                            uint32_t* __restrict__ batch_nruns) {
+  using BRS = cub::BlockRadixSort<uint32_t, kRunThreads, kRunItems, int32_t>;
+  using BScan = cub::BlockScan<int, kRunThreads>;
+  __shared__ union {
+    typename BRS::TempStorage sort;
+    typename BScan::TempStorage scan;
+    uint32_t keys[kRunThreads * kRunItems];
+  } sm;
+  __shared__ int32_t s_q[kRunThreads * kRunItems];
+  const int64_t batch = blockIdx.x;
+  if (batch >= n_batches) return;
+  const int tid = threadIdx.x;
+  const int64_t row0 = batch * B;
+  const int64_t rowN = min(n_r, row0 + B);
+  const int64_t e0 = indptr[row0], e1 = indptr[rowN];
+  const int64_t ne = e1 - e0;
+  if (ne > kRunThreads * kRunItems) {
+    if (tid < 32) warp_merge_runs(batch, tid, indptr, indices, values, rdt, n_r, d, B, sigma, runs_f, runs_q, batch_nruns);
+    return;
+  }
+  // key = feature << 3 | row-in-batch (entries with feature >= d sort last and are dropped)
+  uint32_t key[kRunItems];
+  int32_t q[kRunItems];
+#pragma unroll
+  for (int it = 0; it < kRunItems; ++it) {
+    const int64_t e = e0 + tid * kRunItems + it;
+    key[it] = 0xFFFFFFFFu;
+    q[it] = 0;
+    if (e < e1) {
+      // row of entry e: rows are few (B <= 8), a linear walk over the batch's indptr is enough
+      int b = 0;
+      while (b + 1 < (int)(rowN - row0) && indptr[row0 + b + 1] <= e) ++b;
+      const int32_t f = indices[e];
+      if (f < d) {
+        key[it] = ((uint32_t)f << 3) | (uint32_t)b;
+        q[it] = quantize(values, rdt, e, sigma[row0 + b]);
+      }
+    }
+  }
+  BRS(sm.sort).Sort(key, q, 0, 27);
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < kRunItems; ++it) {
+    sm.keys[tid * kRunItems + it] = key[it];
+    s_q[tid * kRunItems + it] = q[it];
+  }
+  __syncthreads();
+  int starts = 0;
+  bool is_start[kRunItems];
+#pragma unroll
+  for (int it = 0; it < kRunItems; ++it) {
+    const int i = tid * kRunItems + it;
+    const uint32_t k = key[it];
+    is_start[it] = k != 0xFFFFFFFFu && (i == 0 || (sm.keys[i - 1] >> 3) != (k >> 3));
+    starts += is_start[it];
+  }
+  __syncthreads();  // sm.keys is overwritten by the scan temp storage
+  uint32_t keys_local[kRunItems];
+#pragma unroll
+  for (int it = 0; it < kRunItems; ++it) keys_local[it] = key[it];
+  int run_idx, total;
+  BScan(sm.scan).ExclusiveSum(starts, run_idx, total);
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < kRunItems; ++it) sm.keys[tid * kRunItems + it] = keys_local[it];
+  __syncthreads();
+  const size_t base = (size_t)e0;
+#pragma unroll
+  for (int it = 0; it < kRunItems; ++it) {
+    if (is_start[it]) {
+      const int i = tid * kRunItems + it;
+      const uint32_t f = keys_local[it] >> 3;
+      uint32_t mask = 0;
+      int32_t qb[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int j = i; j < kRunThreads * kRunItems && j < i + 8; ++j) {
+        const uint32_t kj = sm.keys[j];
+        if (kj == 0xFFFFFFFFu || (kj >> 3) != f) break;
+        mask |= 1u << (kj & 7u);
+        qb[kj & 7u] = s_q[j];
+      }
+      const size_t run = base + run_idx;
+      runs_f[run] = f | (mask << 24);
+      for (int b = 0; b < B; ++b) runs_q[run * B + b] = qb[b];
+      ++run_idx;
+    }
+  }
+  if (tid == 0) batch_nruns[batch] = (uint32_t)total;
 }
 
 // -------------------------------------------------------------------------- block-wide scan helper
@@ -189,19 +292,24 @@ __host__ __device__ inline size_t acc_region_bytes(int B, int T, int k, int NW) 
 // 8-warp CTAs so that two CTAs with B = 3 fit on one SM, 512 for 16-warp CTAs).
 __host__ __device__ constexpr int kcap(int NW) { return NW == 8 ? 384 : 512; }
 __host__ __device__ inline size_t staging_at(int B, int T, int k, int NW) { return acc_region_bytes(B, T, k, NW); }
-// Head tables: lut[16 groups][B][16] u32 (entry m of group g, row b = sum of q over the set bits of m among
-// head slots 4g..4g+3) and head_mask[B] u64 (head slots present in row b).  The per-slot q values they are
-// built from (q_head[kMaxHead][B]) alias the staging area, which is free during batch setup.
+// Head tables: lut[kMaxHead/4 groups][B][16] u32 (entry m of group g, row b = sum of q over the set bits of
+// m among head slots 4g..4g+3), cum[B][kMaxHead+1] u32 (cum[b][p] = sum of the p largest head q of row b:
+// an upper bound of the head part of any score whose S row shares p head features with r_b) and
+// head_mask[B] u32 (head slots present in row b).  The per-slot q values they are built from
+// (q_head[kMaxHead][B]) alias the staging area, which is free during batch setup.
 __host__ __device__ inline size_t head_at(int B, int T, int k, int NW) {
   return align_up(staging_at(B, T, k, NW) + (size_t)kcap(NW) * B * 4 + (size_t)kcap(NW) * 8 +
                       (size_t)(kcap(NW) + 1) * 4, 16);
 }
-__host__ __device__ inline size_t head_bytes(int B) { return (size_t)(kMaxHead / 4) * B * 16 * 4 + (size_t)B * 8; }
+__host__ __device__ inline size_t head_bytes(int B) {
+  return (size_t)(kMaxHead / 4) * B * 16 * 4 + (size_t)B * (kMaxHead + 1) * 4 + (size_t)B * 4;
+}
 __host__ __device__ inline size_t tail_at(int B, int T, int k, int NW) {
   return align_up(head_at(B, T, k, NW) + head_bytes(B), 16);
 }
 __host__ __device__ inline size_t smem_bytes(int B, int T, int k, int NW) {
-  return tail_at(B, T, k, NW) + (size_t)NW * 8 /* scan partials */ + (size_t)B * NW * 8 /* theta */ + 32 /* misc */;
+  return tail_at(B, T, k, NW) + (size_t)NW * 8 /* scan partials */ + (size_t)B * 8 /* theta */ +
+         (size_t)NW * 32 * 4 /* completion queues */ + 32 /* misc */;
 }
 
 __device__ __forceinline__ void red_add_shared(uint32_t addr, uint32_t v) {
@@ -225,15 +333,17 @@ __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
   uint32_t* s_ustart = (uint32_t*)(s_q + kCap * QS);
   uint32_t* s_fm = s_ustart + kCap;
   uint32_t* s_P = s_fm + kCap;
-  uint32_t* s_lut = (uint32_t*)(smem + head_at(B, T, p.k, NW));  // [16][B][16]
-  uint64_t* s_hmask = (uint64_t*)(s_lut + (kMaxHead / 4) * B * 16);  // [B]
+  uint32_t* s_lut = (uint32_t*)(smem + head_at(B, T, p.k, NW));  // [kMaxHead/4][B][16]
+  uint32_t* s_cum = s_lut + (kMaxHead / 4) * B * 16;                 // [B][kMaxHead + 1]
+  uint32_t* s_hmask = s_cum + B * (kMaxHead + 1);                    // [B]
   int32_t* s_qh = s_q;                                                // [kMaxHead][B], aliases staging
   static_assert(kMaxHead * B <= kcap(NW) * B, "q_head must fit in the staging area");
   uint64_t* s_warp = (uint64_t*)(smem + tail_at(B, T, p.k, NW));
-  uint64_t* s_theta = s_warp + NW;    // [B][NW]: k-th key of each warp's list per row (no atomics needed)
-  int* s_misc = (int*)(s_theta + B * NW);  // [0] batch, [1] n sparse items, [2] TOT, [3] window counter
+  uint64_t* s_theta = s_warp + NW;           // [B]: max over warps of their k-th key per row
+  int* s_misc = (int*)((uint32_t*)(s_theta + B) + NW * 32);  // [0] batch, [1] n sparse items, [2] TOT, [3] window counter
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t* s_queue = (uint32_t*)(s_theta + B) + warp * 32;  // this warp's head-completion queue
   const int k = p.k;
   constexpr bool wint8 = SINT8;
   const bool timing = p.phase != nullptr && tid == 0;
@@ -246,7 +356,7 @@ __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
       t_mark = now;
     }
   };
-  unsigned long long n_visits = 0, n_inserts = 0;
+  unsigned long long n_visits = 0, n_inserts = 0, n_complete = 0, n_skipped = 0;
   const int n_head = p.head_feat[kMaxHead];
   const int n_groups = (n_head + 3) >> 2;
 
@@ -262,7 +372,7 @@ __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
     const int nb = (int)min((int64_t)B, p.n_r - row0);
     const int64_t run_base = p.r_indptr[row0];
     const int nruns = (int)p.batch_nruns[batch];
-    if (tid < B * NW) s_theta[tid] = kKeyFloor;
+    if (tid < B) s_theta[tid] = kKeyFloor;
 
     uint64_t L[B][KS];
     uint64_t own[B];
@@ -286,7 +396,7 @@ __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
           for (int b = 0; b < B; ++b) s_qh[sl * B + b] = p.runs_q[run * B + b];
 #pragma unroll
           for (int b = 0; b < B; ++b)
-            if (fm & (1u << (24 + b))) atomicOr((unsigned long long*)&s_hmask[b], 1ull << sl);
+            if (fm & (1u << (24 + b))) atomicOr(&s_hmask[b], 1u << sl);
         }
       }
       __syncthreads();
@@ -297,6 +407,27 @@ __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
         for (int j = 0; j < 4; ++j)
           if (m & (1 << j)) v += (uint32_t)s_qh[(4 * g + j) * B + b];
         s_lut[i] = v;
+      }
+      if (warp < B) {  // cum[b]: prefix sums of row b's head q sorted descending (warp bitonic sort)
+        uint32_t x = (uint32_t)s_qh[lane * B + warp];
+#pragma unroll
+        for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+          for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+            const uint32_t y = __shfl_xor_sync(0xffffffffu, x, jj);
+            const bool up = (lane & kk) == 0;           // descending overall
+            const bool lower = (lane & jj) == 0;
+            x = (lower == up) ? max(x, y) : min(x, y);
+          }
+        }
+        uint32_t incl = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        s_cum[warp * (kMaxHead + 1) + lane + 1] = incl;
+        if (lane == 0) s_cum[warp * (kMaxHead + 1)] = 0;
       }
     }
     __syncthreads();
@@ -446,91 +577,172 @@ __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
         }
       }
       // -------------------------------------------------------------------- scan + top-k (a5)
-      // warp w owns columns [w*T/NW, (w+1)*T/NW); per 128-column step every lane reads 4 scores of each row,
-      // adds the head features from the batch's lookup tables (one table read per 4 head features per
-      // row and column), zero-fills, and offers keys above theta to the warp's register top-k list.
+      // warp w owns columns [w*T/NW, (w+1)*T/NW); per 128-column step every lane reads the 4 accumulated
+      // scores (id-list features) of each row and offers keys above theta to the warp's register top-k list
+      // of that row, then zero-fills.  With head features the accumulated score is only part of the score:
+      // it is completed exactly, from the lookup tables, only where the upper bound
+      //     acc + cum[b][popc(head bits of s & head mask of r_b)]   (the largest head weights of r_b)
+      // reaches theta (the threshold refinement of IIIB) -- a pair whose bound is below
+      // theta cannot enter the top-k, so skipping its completion changes nothing.
       {
         const int cols = T / NW;
         const int cbase = warp * cols;
         const uint32_t gbase = (uint32_t)(p.s_id_base + t * (int64_t)T);
-        const uint64_t* hcols = p.head_cols + (size_t)t * T + cbase + lane * 4;
-        ulonglong2 hA = make_ulonglong2(0, 0), hB = make_ulonglong2(0, 0);
-        if (n_groups) {
-          hA = __ldg((const ulonglong2*)hcols);
-          hB = __ldg((const ulonglong2*)(hcols + 2));
-        }
-        // theta of row b = max over the warps' k-th keys: k keys at least that large exist in one list, so
-        // any candidate key below it cannot be in the row's final top-k (reading c1 total order)
+        const uint32_t* hcols = p.head_cols + (size_t)t * T + cbase + lane * 4;
+        uint4 hq = make_uint4(0, 0, 0, 0);
+        if (n_groups) hq = __ldg((const uint4*)hcols);
+        // theta of row b = max over the warps' k-th keys (k keys at least that large exist in one list, so a
+        // candidate key below it cannot be in the row's final top-k; reading c1 total order)
         auto row_theta = [&](int b) {
-          const volatile uint64_t* tb = s_theta + b * NW;
-          uint64_t m = own[b];
-#pragma unroll
-          for (int w = 0; w < NW; ++w) m = max(m, (uint64_t)tb[w]);
-          return m;
+          const uint64_t sh = *(volatile uint64_t*)&s_theta[b];
+          return sh > own[b] ? sh : own[b];
+        };
+        // cheap superset test: key > theta needs score >= t32 (theta's score, +1 when theta's id part admits
+        // no id); the exact 64-bit key comparison happens in list_offer_lanes
+        auto t32_of = [](uint64_t th) {
+          return (uint32_t)(th >> 32) + ((uint32_t)th == 0xFFFFFFFFu ? 1u : 0u);
+        };
+        auto publish = [&](int b) {
+          const uint64_t nk = list_kth<KS>(L[b], k);
+          if (nk > own[b]) {
+            own[b] = nk;
+            if (lane == 0) atomicMax((unsigned long long*)&s_theta[b], (unsigned long long)nk);
+          }
         };
         uint64_t th[B];
 #pragma unroll
         for (int b = 0; b < B; ++b) th[b] = row_theta(b);
         for (int c = 0; c < cols; c += 128) {
           const int col = cbase + c + lane * 4;
+          const uint32_t g0 = gbase + (uint32_t)col;
           uint32_t v[B][4];
 #pragma unroll
           for (int b = 0; b < B; ++b) {
             if (b < nb) {
               const uint4 x = *(const uint4*)(acc + (size_t)b * TS + col);
-              *(uint4*)(acc + (size_t)b * TS + col) = make_uint4(0, 0, 0, 0);
               v[b][0] = x.x; v[b][1] = x.y; v[b][2] = x.z; v[b][3] = x.w;
             } else {
               v[b][0] = v[b][1] = v[b][2] = v[b][3] = 0;
             }
           }
+          bool plain = n_groups == 0;
           if (n_groups) {
-            const uint64_t hw[4] = {hA.x, hA.y, hB.x, hB.y};
-            if (c + 128 < cols) {  // next step's head words in flight while this step's tables are read
-              hA = __ldg((const ulonglong2*)(hcols + c + 128));
-              hB = __ldg((const ulonglong2*)(hcols + c + 130));
-            }
-            for (int g = 0; g < n_groups; ++g) {
-              const uint32_t* lutg = s_lut + g * B * 16;
+            const uint32_t hw[4] = {hq.x, hq.y, hq.z, hq.w};
+            if (c + 128 < cols) hq = __ldg((const uint4*)(hcols + c + 128));  // next step's head words
+            uint32_t pend = 0;  // bit 4b+j: pair (row b, column col+j) may reach theta
 #pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const uint32_t m = (uint32_t)(hw[j] >> (4 * g)) & 15u;
-#pragma unroll
-                for (int b = 0; b < B; ++b) v[b][j] += lutg[b * 16 + m];
-              }
-            }
-            if (p.counters) {
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-#pragma unroll
-                for (int b = 0; b < B; ++b) n_visits += __popcll(hw[j] & s_hmask[b]);
-            }
-          }
-          const uint32_t g0 = gbase + (uint32_t)col;
-#pragma unroll
-          for (int b = 0; b < B; ++b) {
-            if (b < nb) {
-              // cheap superset test: key > theta needs score >= theta's score (+1 when theta's id part admits
-              // no id); the exact 64-bit key comparison happens in list_offer_lanes
-              const uint32_t thh = (uint32_t)(th[b] >> 32);
-              const uint32_t t32 = thh + ((uint32_t)th[b] == 0xFFFFFFFFu ? 1u : 0u);
-              const bool any = (v[b][0] >= t32) | (v[b][1] >= t32) | (v[b][2] >= t32) | (v[b][3] >= t32);
-              if (__any_sync(0xffffffffu, any) && t32 != 0u) {
+            for (int b = 0; b < B; ++b) {
+              if (b < nb) {
                 th[b] = row_theta(b);
+                const uint32_t t32 = t32_of(th[b]);
+                const uint32_t hm = s_hmask[b];
+                const uint32_t* cum = s_cum + b * (kMaxHead + 1);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                  const uint64_t key = v[b][j] ? make_key(v[b][j], g0 + j) : 0;
-                  int n = list_offer_lanes<KS>(L[b], key, th[b], k, lane);
-                  n_inserts += (lane == 0) ? n : 0;
+                  const uint32_t nh = __popc(hw[j] & hm);
+                  const bool need = v[b][j] + cum[nh] >= t32;
+                  if (need) pend |= 1u << (4 * b + j);
+                  if (p.counters) {
+                    n_visits += nh;
+                    n_complete += need;
+                    n_skipped += need ? 0u : nh;
+                  }
                 }
-                const uint64_t nk = list_kth<KS>(L[b], k);
-                if (nk > own[b]) {
-                  own[b] = nk;
-                  if (lane == 0) s_theta[b * NW + warp] = nk;
+              }
+            }
+            const int npend = __reduce_add_sync(0xffffffffu, __popc(pend));
+            if (npend > 64) {
+              // many pairs may reach theta (the first tiles of a batch, theta still low): complete every pair
+              // from the tables and take the plain filter below
+#pragma unroll 1
+              for (int g = 0; g < n_groups; ++g) {
+                const uint32_t* lutg = s_lut + g * B * 16;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const uint32_t m = (hw[j] >> (4 * g)) & 15u;
+#pragma unroll
+                  for (int b = 0; b < B; ++b) v[b][j] += lutg[b * 16 + m];
+                }
+              }
+              plain = true;
+            } else if (npend) {
+              // exact completion, 32 pending pairs of the warp at a time: compact (lane, pair) into the queue,
+              // then lane l completes entry l
+              uint32_t touched = 0;
+              const uint32_t* wcols = p.head_cols + (size_t)t * T + cbase + c;
+              do {
+                const int cnt = __popc(pend);
+                int excl = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                  const int y = __shfl_up_sync(0xffffffffu, excl, o);
+                  if (lane >= o) excl += y;
+                }
+                const int total = __shfl_sync(0xffffffffu, excl, 31);
+                excl -= cnt;
+                for (int e = excl; e < 32 && pend; ++e) {
+                  const int i = __ffs(pend) - 1;
+                  pend &= pend - 1;
+                  s_queue[e] = ((uint32_t)lane << 4) | (uint32_t)i;
+                }
+                __syncwarp();
+                uint64_t key = 0;
+                int pb = -1;
+                if (lane < min(total, 32)) {
+                  const uint32_t ent = s_queue[lane];
+                  const int i = ent & 15;
+                  pb = i >> 2;
+                  const int cl = (int)(ent >> 4) * 4 + (i & 3);  // column within this 128-column step
+                  const uint32_t w = __ldg(wcols + cl);
+                  uint32_t sc = acc[(size_t)pb * TS + cbase + c + cl];
+                  const uint32_t* lutb = s_lut + pb * 16;
+                  for (int g = 0; g < n_groups; ++g) sc += lutb[g * B * 16 + ((w >> (4 * g)) & 15u)];
+                  uint64_t thb = th[0];
+#pragma unroll
+                  for (int b = 1; b < B; ++b)
+                    if (pb == b) thb = th[b];
+                  key = make_key(sc, gbase + (uint32_t)(cbase + c + cl));
+                  if (!(sc && key > thb)) key = 0;  // the exact score does not beat this row's theta
+                }
+                __syncwarp();
+                if (__ballot_sync(0xffffffffu, key != 0)) {
+#pragma unroll
+                  for (int b = 0; b < B; ++b) {
+                    if (__ballot_sync(0xffffffffu, key != 0 && pb == b)) {
+                      const int n = list_offer_lanes<KS>(L[b], pb == b ? key : 0, th[b], k, lane);
+                      n_inserts += (lane == 0) ? n : 0;
+                      touched |= (n ? 1u : 0u) << b;
+                    }
+                  }
+                }
+              } while (__any_sync(0xffffffffu, pend != 0));
+#pragma unroll
+              for (int b = 0; b < B; ++b)
+                if (touched & (1u << b)) publish(b);
+            }
+          }
+          if (plain) {
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+              if (b < nb) {
+                const uint32_t t32 = t32_of(th[b]);
+                const bool any = (v[b][0] >= t32) | (v[b][1] >= t32) | (v[b][2] >= t32) | (v[b][3] >= t32);
+                if (__any_sync(0xffffffffu, any) && t32 != 0u) {
+                  th[b] = row_theta(b);
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) {
+                    const uint64_t key = v[b][j] ? make_key(v[b][j], g0 + j) : 0;
+                    int n = list_offer_lanes<KS>(L[b], key, th[b], k, lane);
+                    n_inserts += (lane == 0) ? n : 0;
+                  }
+                  publish(b);
                 }
               }
             }
           }
+#pragma unroll
+          for (int b = 0; b < B; ++b)
+            if (b < nb) *(uint4*)(acc + (size_t)b * TS + col) = make_uint4(0, 0, 0, 0);
         }
         __syncthreads();
         phase_mark(3);
@@ -575,10 +787,14 @@ __global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
     for (int o = 16; o; o >>= 1) {
       n_visits += __shfl_xor_sync(0xffffffffu, n_visits, o);
       n_inserts += __shfl_xor_sync(0xffffffffu, n_inserts, o);
+      n_complete += __shfl_xor_sync(0xffffffffu, n_complete, o);
+      n_skipped += __shfl_xor_sync(0xffffffffu, n_skipped, o);
     }
     if (lane == 0) {
       atomicAdd(&p.counters[0], n_visits);
       atomicAdd(&p.counters[1], n_inserts);
+      atomicAdd(&p.counters[2], n_skipped);
+      atomicAdd(&p.counters[3], n_complete);
     }
   }
 }
@@ -777,9 +993,20 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_row_scale");
   {
     int64_t threads = n_batches * 32;
-    k_build_runs<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(R->indptr, R->indices, R->values, R->dtype,
-                                                                   R->n_rows, idx->d, B, n_batches, sigma, runs_f,
-                                                                   runs_q, nruns);
+    // block-sort capacity from the mean entries per batch (x1.5 headroom); larger batches use the warp merge
+    const double mean = (double)R->nnz / (double)n_batches * 1.5;
+    if (mean <= kRunThreads * 4)
+      k_build_runs<4><<<(unsigned)n_batches, kRunThreads, 0, st>>>(R->indptr, R->indices, R->values, R->dtype, R->n_rows,
+                                                                   idx->d, B, n_batches, sigma, runs_f, runs_q, nruns);
+    else if (mean <= kRunThreads * 8)
+      k_build_runs<8><<<(unsigned)n_batches, kRunThreads, 0, st>>>(R->indptr, R->indices, R->values, R->dtype, R->n_rows,
+                                                                   idx->d, B, n_batches, sigma, runs_f, runs_q, nruns);
+    else if (mean <= kRunThreads * 16)
+      k_build_runs<16><<<(unsigned)n_batches, kRunThreads, 0, st>>>(R->indptr, R->indices, R->values, R->dtype, R->n_rows,
+                                                                    idx->d, B, n_batches, sigma, runs_f, runs_q, nruns);
+    else
+      k_build_runs<32><<<(unsigned)n_batches, kRunThreads, 0, st>>>(R->indptr, R->indices, R->values, R->dtype, R->n_rows,
+                                                                    idx->d, B, n_batches, sigma, runs_f, runs_q, nruns);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_build_runs");
   }
   QP p;

@@ -44,8 +44,8 @@ def test_index_bytes_host_only():
     at = al(4 * n_off)          # off
     at = al(at + 4 * 10_000)    # df
     at = al(at + 4 * 10_000)    # head_slot
-    at = al(at + 4 * 65)        # head_feat + n_head
-    at = al(at + 8 * nt * 8192)  # head_cols
+    at = al(at + 4 * 33)        # head_feat + n_head
+    at = al(at + 4 * nt * 8192)  # head_cols
     assert n == al(at + 16 * cap)
 
 

@@ -168,10 +168,10 @@ def test_index_layout_matches_scipy_csc(name, T, hd):
     hs_at = al(df_at + 4 * c.d)
     head_slot = raw[hs_at:hs_at + 4 * c.d].view(np.int32)
     hf_at = al(hs_at + 4 * c.d)
-    head_feat = raw[hf_at:hf_at + 4 * 65].view(np.int32)
-    hc_at = al(hf_at + 4 * 65)
-    head_cols = raw[hc_at:hc_at + 8 * NT * T].view(np.uint64)
-    ids_at = al(hc_at + 8 * NT * T)
+    head_feat = raw[hf_at:hf_at + 4 * 33].view(np.int32)
+    hc_at = al(hf_at + 4 * 33)
+    head_cols = raw[hc_at:hc_at + 4 * NT * T].view(np.uint32)
+    ids_at = al(hc_at + 4 * NT * T)
     cap = st["unit_capacity"]
     ids = raw[ids_at:ids_at + 16 * cap].view(np.uint16)
     vals = None
@@ -180,7 +180,7 @@ def test_index_layout_matches_scipy_csc(name, T, hd):
         vals = raw[vals_at:vals_at + 8 * cap].view(np.uint8)
     want_df = np.bincount(S.indices, minlength=c.d)
     np.testing.assert_array_equal(df, want_df)
-    n_head = int(head_feat[64])
+    n_head = int(head_feat[32])
     heads = head_feat[:n_head]
     if name == "C5":
         assert n_head == 0
@@ -195,7 +195,7 @@ def test_index_layout_matches_scipy_csc(name, T, hd):
     M = sp.csr_matrix((data, S.indices, S.indptr), shape=(S.n_rows, c.d)).tocsc()
     # head words: bit i of head_cols[s] <=> s has heads[i]
     for i, f in enumerate(heads):
-        bits = ((head_cols[:S.n_rows] >> np.uint64(i)) & np.uint64(1)).astype(bool)
+        bits = ((head_cols[:S.n_rows] >> np.uint32(i)) & np.uint32(1)).astype(bool)
         want = np.zeros(S.n_rows, bool)
         want[M[:, f].indices] = True
         np.testing.assert_array_equal(bits, want)
@@ -259,3 +259,12 @@ def test_multi_chunk_batches(cta_warps, batch_rows):
     nR = np.bincount(R.indices, minlength=d)
     nS = np.bincount(S.indices, minlength=d)
     assert int(cnt[0]) == int((nR.astype(np.int64) * nS).sum())
+
+
+def test_wide_rows_fallback_run_merge():
+    """Batches with more (row, feature) entries than the block sort holds (4096) use the warp merge."""
+    rng = np.random.default_rng(11)
+    d = 3000
+    R = random_csr(rng, 9, d, 1300, 1500, "int8", vmax=5)
+    S = random_csr(rng, 4000, d, 100, 300, "int8", vmax=5)
+    _check(R, S, 20, tile=2048, batch_rows=4, cta_warps=8)
