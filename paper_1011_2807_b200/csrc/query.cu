@@ -288,9 +288,9 @@ __host__ __device__ inline size_t acc_region_bytes(int B, int T, int k, int NW) 
 }
 
 // shared-memory layout of k_accumulate_topk<B, ., ., NW>; the kernel derives its pointers from the same sums.
-// Staging of one chunk of runs: q[cap][B], ustart[cap], fm[cap], P[cap + 1]; cap = runs per chunk (384 for
-// 8-warp CTAs so that two CTAs with B = 3 fit on one SM, 512 for 16-warp CTAs).
-__host__ __device__ constexpr int kcap(int NW) { return NW == 8 ? 384 : 512; }
+// Staging of one chunk of runs: q[cap][B], ustart[cap], fm[cap], P[cap + 1]; cap = runs per chunk (320 for
+// 8-warp CTAs so that three CTAs with B = 2 fit on one SM, 512 for 16-warp CTAs).
+__host__ __device__ constexpr int kcap(int NW) { return NW == 8 ? 320 : 512; }
 __host__ __device__ inline size_t staging_at(int B, int T, int k, int NW) { return acc_region_bytes(B, T, k, NW); }
 // Head tables: lut[kMaxHead/4 groups][B][16] u32 (entry m of group g, row b = sum of q over the set bits of
 // m among head slots 4g..4g+3), cum[B][kMaxHead+1] u32 (cum[b][p] = sum of the p largest head q of row b:
@@ -319,7 +319,7 @@ __device__ __forceinline__ void red_add_shared(uint32_t addr, uint32_t v) {
 constexpr int kWinChunk = 8;  // 32-unit windows a warp takes per grab of the dynamic window counter
 
 template <int B, int KS, bool SINT8, int NW>
-__global__ void __launch_bounds__(NW * 32) k_accumulate_topk(QP p) {
+__global__ void __launch_bounds__(NW * 32, NW == 8 ? 3 : 1) k_accumulate_topk(QP p) {
   constexpr int NT_ = NW * 32;        // threads per CTA
   constexpr int kCap = kcap(NW);      // runs staged per chunk
   constexpr int IPT = (kCap + NT_ - 1) / NT_;  // staged runs per thread (the last may be partial)
@@ -816,7 +816,8 @@ bool shape_supported(int B, int NW, int KS) {
 }
 
 // pick (B rows per batch, NW warps per CTA): an explicit request must fit; auto prefers 8-warp CTAs with
-// two resident per SM (barrier stalls of one overlap the other), then 16-warp CTAs, largest B first.
+// three (then two) resident per SM -- barrier and latency stalls of one overlap the others -- then one
+// 16-warp CTA, largest B first.
 bool pick_shape(int T, int k, int req_B, int req_NW, Shape* out) {
   const int KS = ks_for_k(k);
   const size_t max_smem = 227 * 1024;
@@ -838,6 +839,8 @@ bool pick_shape(int T, int k, int req_B, int req_NW, Shape* out) {
     }
     return false;
   }
+  for (int B : Bs)
+    if (B >= 2 && fits(B, 8, 3)) { *out = {B, 8}; return true; }
   for (int B : Bs)
     if (B >= 3 && fits(B, 8, 2)) { *out = {B, 8}; return true; }
   for (int B : Bs)
