@@ -268,3 +268,20 @@ def test_wide_rows_fallback_run_merge():
     R = random_csr(rng, 9, d, 1300, 1500, "int8", vmax=5)
     S = random_csr(rng, 4000, d, 100, 300, "int8", vmax=5)
     _check(R, S, 20, tile=2048, batch_rows=4, cta_warps=8)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name,n_sample", [("C2", 64), ("C3", 24), ("C4", 12), ("C5", 16)])
+def test_full_size_sampled_rows(name, n_sample):
+    """BASELINE.json full sizes, in the launch configuration bench.py times (default tile, auto batch shape):
+    every row is computed on the GPU; a seeded sample of rows (first, last and random) is checked against the
+    oracle, one row at a time against all of S."""
+    import os
+    c = gen.CONFIGS[name]
+    R, S = gen.generate(c, "R"), gen.generate(c, "S")
+    g_ids, g_sc = gpu_join(R, S, c.k)
+    rng = np.random.default_rng(2024)
+    rows = np.unique(np.concatenate([[0, R.n_rows - 1], rng.choice(R.n_rows, n_sample - 2, replace=False)]))
+    threads = max(1, min(len(rows), len(os.sched_getaffinity(0))))
+    o_ids, o_sc = oracle.knn(R, S, c.k, rows=rows, threads=threads)
+    assert_parity(R.take_rows(rows), S, g_ids[rows], g_sc[rows], o_ids, o_sc, rows=None)
