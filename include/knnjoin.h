@@ -79,8 +79,11 @@ typedef struct {
 
 /* Query options (all optional; pass NULL for defaults).
  *  batch_rows: R rows per CTA batch (0 = auto).
- *  cta_warps:  warps per CTA of the accumulation kernel, 8 or 16 (0 = auto: 8-warp CTAs, two per SM,
- *              with the largest batch whose score arrays fit; else one 16-warp CTA per SM).
+ *  cta_warps:  warps per CTA of the accumulation kernel, 8 or 16 (0 = auto: 8-warp CTAs, three or two per
+ *              SM, with the largest batch whose score arrays fit; else one 16-warp CTA per SM).
+ *  tiles_per_pass: S tiles swept by all batches before any batch moves on (0 = auto: about a third of the
+ *              L2 cache worth of index per pass; the whole index when it fits).  Top-k state is carried
+ *              between passes in the workspace; results do not depend on it.
  *  counters:   NULL, or a device int64_t[4] that the query ADDS into: [0] postings visited (Eq. 4 second
  *              term; head postings are counted whether or not their completion is skipped),
  *              [1] candidate inserts into the top-k lists, [2] head postings whose exact addition was skipped
@@ -98,6 +101,7 @@ typedef struct {
   void* ev_end;
   int64_t* phase_cycles;
   int32_t cta_warps;
+  int32_t tiles_per_pass;
 } knnjoin_query_options;
 
 typedef struct knnjoin_index knnjoin_index; /* opaque HOST handle; borrows the caller's index storage */

@@ -52,6 +52,10 @@ struct QP {
   const uint32_t* batch_nruns;
   const double* inv_sigma;
   uint32_t* batch_counter;
+  int64_t tiles_per_pass;   // S tiles per pass: all batches sweep pass 0, then pass 1, ... (L2 locality)
+  int64_t n_passes;
+  uint64_t* state_keys;     // [n_r][k] top-k keys carried between passes (n_passes > 1)
+  uint32_t* pass_done;      // [n_batches] number of passes finished per batch
   unsigned long long* counters;
   unsigned long long* phase;  // [8] cycles per phase (profiling), or nullptr
   // out
@@ -362,17 +366,33 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 3 : 1) k_accumulate_topk(QP
 
   for (int i = tid; i < (int)(acc_region_bytes(B, T, k, NW) / 16); i += NT_) ((uint4*)acc)[i] = make_uint4(0, 0, 0, 0);
 
+  // Work items are (pass, batch) in pass-major order: every CTA sweeps the tiles of one pass (a slab of the
+  // index sized to stay L2-resident) over all batches before any moves to the next pass.  A batch's top-k
+  // keys are carried between its passes in global memory (state_keys); item (pass g, batch b) waits until
+  // item (g - 1, b) -- fetched earlier, so already running or done -- has published them.
+  const int64_t n_items = p.n_batches * p.n_passes;
   for (;;) {
     __syncthreads();
     if (tid == 0) s_misc[0] = (int)atomicAdd(p.batch_counter, 1u);
     __syncthreads();
-    const int64_t batch = s_misc[0];
-    if (batch >= p.n_batches) break;
+    const int64_t item = s_misc[0];
+    if (item >= n_items) break;
+    const int64_t pass = item / p.n_batches;
+    const int64_t batch = item - pass * p.n_batches;
+    const int64_t t_begin = pass * p.tiles_per_pass;
+    const int64_t t_end = min(p.NT, t_begin + p.tiles_per_pass);
+    const bool last_pass = pass == p.n_passes - 1;
     const int64_t row0 = batch * B;
     const int nb = (int)min((int64_t)B, p.n_r - row0);
     const int64_t run_base = p.r_indptr[row0];
     const int nruns = (int)p.batch_nruns[batch];
-    if (tid < B) s_theta[tid] = kKeyFloor;
+    if (pass > 0) {
+      if (tid == 0) {
+        while (*(volatile uint32_t*)&p.pass_done[batch] < (uint32_t)pass) __nanosleep(200);
+        __threadfence();
+      }
+      __syncthreads();
+    }
 
     uint64_t L[B][KS];
     uint64_t own[B];
@@ -381,6 +401,18 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 3 : 1) k_accumulate_topk(QP
       own[b] = kKeyFloor;
 #pragma unroll
       for (int s = 0; s < KS; ++s) L[b][s] = 0;
+      if (pass > 0 && warp == 0 && b < nb) {  // warp 0 resumes from the batch's merged list
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+          const int pos = s * 32 + lane;
+          if (pos < k) L[b][s] = __ldcg((const unsigned long long*)p.state_keys + (size_t)(row0 + b) * k + pos);
+        }
+        own[b] = list_kth<KS>(L[b], k);
+      }
+    }
+    if (warp == 0 && lane == 0) {
+#pragma unroll
+      for (int b = 0; b < B; ++b) s_theta[b] = own[b];
     }
     // ------------------------------------------------------------------ head tables of this batch
     if (n_groups) {
@@ -433,8 +465,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 3 : 1) k_accumulate_topk(QP
     __syncthreads();
     phase_mark(5);
 
-    const int64_t ntiles = nruns > 0 ? p.NT : 0;
-    for (int64_t t = 0; t < ntiles; ++t) {
+    const int64_t t_stop = nruns > 0 ? t_end : t_begin;
+    for (int64_t t = t_begin; t < t_stop; ++t) {
       for (int c0 = 0; c0 < nruns; c0 += kCap) {
         // ---------------------------------------------------------------- stage chunk of runs
         // non-empty slices are compacted with their position P in the flattened unit stream (head
@@ -771,9 +803,21 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 3 : 1) k_accumulate_topk(QP
           }
         }
         const int64_t r = row0 + warp;
-        list_finalize<KS>(M, k, r, p.inv_sigma[r], p.out_keys, p.out_ids, p.out_scores, lane);
+        if (last_pass) {
+          list_finalize<KS>(M, k, r, p.inv_sigma[r], p.out_keys, p.out_ids, p.out_scores, lane);
+        } else {
+#pragma unroll
+          for (int s = 0; s < KS; ++s) {
+            const int pos = s * 32 + lane;
+            if (pos < k) __stcg((unsigned long long*)p.state_keys + (size_t)r * k + pos, (unsigned long long)M[s]);
+          }
+        }
       }
       __syncthreads();
+      if (!last_pass && tid == 0) {
+        __threadfence();
+        atomicExch(&p.pass_done[batch], (uint32_t)(pass + 1));
+      }
       for (int i = tid; i < NW * B * k; i += NT_) scratch[i] = 0;
       phase_mark(4);
     }
@@ -801,7 +845,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 3 : 1) k_accumulate_topk(QP
 
 // ------------------------------------------------------------------------------------ host dispatch
 struct QueryWs {
-  size_t sigma_at, inv_at, runs_f_at, runs_q_at, nruns_at, counter_at, total;
+  size_t sigma_at, inv_at, runs_f_at, runs_q_at, nruns_at, counter_at, state_at, done_at, total;
 };
 
 struct Shape {
@@ -850,7 +894,7 @@ bool pick_shape(int T, int k, int req_B, int req_NW, Shape* out) {
   return false;
 }
 
-bool query_ws_layout(int64_t n_r, int64_t nnz_r, int B, QueryWs* W) {
+bool query_ws_layout(int64_t n_r, int64_t nnz_r, int B, int k, QueryWs* W) {
   int64_t n_batches = (n_r + B - 1) / B;
   size_t at = 0;
   W->sigma_at = at;   at = align_up(at + 8 * (size_t)n_r, 256);
@@ -859,6 +903,8 @@ bool query_ws_layout(int64_t n_r, int64_t nnz_r, int B, QueryWs* W) {
   W->runs_q_at = at;  at = align_up(at + 4 * (size_t)nnz_r * B, 256);
   W->nruns_at = at;   at = align_up(at + 4 * (size_t)n_batches, 256);
   W->counter_at = at; at = align_up(at + 16, 256);
+  W->state_at = at;   at = align_up(at + 8 * (size_t)n_r * k, 256);
+  W->done_at = at;    at = align_up(at + 4 * (size_t)n_batches, 256);
   W->total = at;
   return true;
 }
@@ -873,7 +919,7 @@ cudaError_t launch_main4(const QP& p, int sms, cudaStream_t st) {
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, sm)) != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   int64_t grid = (int64_t)sms * per_sm;
-  if (grid > p.n_batches) grid = p.n_batches;
+  if (grid > p.n_batches * p.n_passes) grid = p.n_batches * p.n_passes;
   kern<<<(unsigned)grid, NW * 32, sm, st>>>(p);
   return cudaGetLastError();
 }
@@ -949,7 +995,7 @@ KJ_API size_t knnjoin_query_workspace_bytes(const knnjoin_index* idx, const knnj
     return 0;
   }
   QueryWs W;
-  query_ws_layout(R->n_rows, R->nnz, sh.B, &W);
+  query_ws_layout(R->n_rows, R->nnz, sh.B, k, &W);
   return W.total;
 }
 
@@ -972,7 +1018,7 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
   }
   const int B = sh.B;
   QueryWs W;
-  query_ws_layout(R->n_rows, R->nnz, B, &W);
+  query_ws_layout(R->n_rows, R->nnz, B, k, &W);
   if (!workspace || workspace_bytes < W.total) { set_error("query workspace %zu < %zu bytes", workspace_bytes, W.total); return KNNJOIN_ERR_WORKSPACE; }
   if ((uintptr_t)workspace & 255) { set_error("workspace must be 256-byte aligned"); return KNNJOIN_ERR_ARG; }
   if (R->n_rows == 0) return KNNJOIN_OK;
@@ -988,10 +1034,13 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
   int32_t* runs_q = (int32_t*)(wb + W.runs_q_at);
   uint32_t* nruns = (uint32_t*)(wb + W.nruns_at);
   uint32_t* counter = (uint32_t*)(wb + W.counter_at);
+  uint64_t* state_keys = (uint64_t*)(wb + W.state_at);
+  uint32_t* pass_done = (uint32_t*)(wb + W.done_at);
   const int32_t smax = idx->s_dtype == KNNJOIN_INT8 ? 127 : 1;
   const int64_t n_batches = (R->n_rows + B - 1) / B;
   cudaError_t e;
   if ((e = cudaMemsetAsync(counter, 0, 16, st)) != cudaSuccess) return cuda_fail(e, "memset counter");
+  if ((e = cudaMemsetAsync(pass_done, 0, 4 * (size_t)n_batches, st)) != cudaSuccess) return cuda_fail(e, "memset pass_done");
   launch_row_scale(R, idx->d, smax, sigma, inv_sigma, st);
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_row_scale");
   {
@@ -1032,6 +1081,23 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
   p.batch_nruns = nruns;
   p.inv_sigma = inv_sigma;
   p.batch_counter = counter;
+  {
+    // tiles per pass: a slab of the index small enough to stay in L2 while every batch sweeps it
+    int dev = 0, l2 = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    int64_t tpp = qopt ? qopt->tiles_per_pass : 0;
+    if (tpp <= 0) {
+      const double per_tile = (double)idx->storage_bytes / (double)(idx->n_tiles > 0 ? idx->n_tiles : 1);
+      tpp = (int64_t)((double)(l2 > 0 ? l2 : (96 << 20)) / 3.0 / (per_tile > 1.0 ? per_tile : 1.0));
+      if (tpp < 1) tpp = 1;
+    }
+    if (tpp > idx->n_tiles) tpp = idx->n_tiles > 0 ? idx->n_tiles : 1;
+    p.tiles_per_pass = tpp;
+    p.n_passes = idx->n_tiles > 0 ? (idx->n_tiles + tpp - 1) / tpp : 1;
+  }
+  p.state_keys = state_keys;
+  p.pass_done = pass_done;
   p.counters = (unsigned long long*)(qopt ? qopt->counters : nullptr);
   p.phase = (unsigned long long*)(qopt ? qopt->phase_cycles : nullptr);
   p.out_keys = out_keys;

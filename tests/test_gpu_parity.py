@@ -285,3 +285,14 @@ def test_full_size_sampled_rows(name, n_sample):
     threads = max(1, min(len(rows), len(os.sched_getaffinity(0))))
     o_ids, o_sc = oracle.knn(R, S, c.k, rows=rows, threads=threads)
     assert_parity(R.take_rows(rows), S, g_ids[rows], g_sc[rows], o_ids, o_sc, rows=None)
+
+
+@pytest.mark.parametrize("name,tpp", [("C2", 1), ("C2", 3), ("C3", 2), ("C5", 1)])
+def test_tile_passes_identical(name, tpp):
+    """Pass-major schedule (top-k state carried between passes in the workspace) == single pass, bit for bit."""
+    c = gen.CONFIGS[name].scaled(60, 20000)
+    R, S = gen.generate(c, "R"), gen.generate(c, "S")
+    ids, sc = _check(R, S, c.k, tile=2048, tiles_per_pass=tpp)
+    ref = gpu_join(R, S, c.k, tile=2048, tiles_per_pass=1000)
+    np.testing.assert_array_equal(ids, ref[0])
+    np.testing.assert_array_equal(sc, ref[1])
