@@ -79,8 +79,11 @@ typedef struct {
 
 /* Query options (all optional; pass NULL for defaults).
  *  batch_rows: R rows per CTA batch (0 = auto).
- *  cta_warps:  warps per CTA of the accumulation kernel, 8 or 16 (0 = auto: 8-warp CTAs, three or two per
- *              SM, with the largest batch whose score arrays fit; else one 16-warp CTA per SM).
+ *  cta_warps:  warps per CTA of the accumulation kernel, 4, 8 or 16.  Auto (batch_rows and cta_warps both
+ *              0): an index without head features gets 4-warp one-row CTAs, six per SM; one with head features
+ *              gets 8-warp CTAs, three (or two) per SM, with the largest batch whose score arrays fit.  To
+ *              choose, the first auto-shaped query on an index reads the index's head count (a 4-byte
+ *              device-to-host copy that synchronises `stream` once per index).
  *  tiles_per_pass: S tiles swept by all batches before any batch moves on (0 = auto: about a third of the
  *              L2 cache worth of index per pass; the whole index when it fits).  Top-k state is carried
  *              between passes in the workspace; results do not depend on it.

@@ -56,6 +56,7 @@ struct knnjoin_index {
   knnjoin_dtype s_dtype = KNNJOIN_BINARY;
   uint32_t head_min_df = 0xFFFFFFFFu;  // df threshold of head features (0xFFFFFFFF: none)
   int32_t head_max = 0;                // cap on head features (0: none)
+  mutable int32_t n_head_host = -1;    // head count, read once by the first auto-shaped query (-1 unknown)
   const uint32_t* off = nullptr;       // [n_off] posting-unit (16 B) offsets, feature-major: f*(n_tiles+1)+t
   const int32_t* df = nullptr;         // [d] |I_d| (document frequency of each feature in S)
   const int32_t* head_slot = nullptr;  // [d] head slot of a feature, -1 if not a head feature

@@ -294,7 +294,7 @@ __host__ __device__ inline size_t acc_region_bytes(int B, int T, int k, int NW) 
 // shared-memory layout of k_accumulate_topk<B, ., ., NW>; the kernel derives its pointers from the same sums.
 // Staging of one chunk of runs: q[cap][B], ustart[cap], fm[cap], P[cap + 1]; cap = runs per chunk (320 for
 // 8-warp CTAs so that three CTAs with B = 2 fit on one SM, 512 for 16-warp CTAs).
-__host__ __device__ constexpr int kcap(int NW) { return NW == 8 ? 320 : 512; }
+__host__ __device__ constexpr int kcap(int NW) { return NW == 4 ? 256 : (NW == 8 ? 320 : 512); }
 __host__ __device__ inline size_t staging_at(int B, int T, int k, int NW) { return acc_region_bytes(B, T, k, NW); }
 // Head tables: lut[kMaxHead/4 groups][B][16] u32 (entry m of group g, row b = sum of q over the set bits of
 // m among head slots 4g..4g+3), cum[B][kMaxHead+1] u32 (cum[b][p] = sum of the p largest head q of row b:
@@ -323,7 +323,7 @@ __device__ __forceinline__ void red_add_shared(uint32_t addr, uint32_t v) {
 constexpr int kWinChunk = 8;  // 32-unit windows a warp takes per grab of the dynamic window counter
 
 template <int B, int KS, bool SINT8, int NW>
-__global__ void __launch_bounds__(NW * 32, NW == 8 ? 3 : 1) k_accumulate_topk(QP p) {
+__global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_accumulate_topk(QP p) {
   constexpr int NT_ = NW * 32;        // threads per CTA
   constexpr int kCap = kcap(NW);      // runs staged per chunk
   constexpr int IPT = (kCap + NT_ - 1) / NT_;  // staged runs per thread (the last may be partial)
@@ -854,6 +854,7 @@ struct Shape {
 
 bool shape_supported(int B, int NW, int KS) {
   if (B * KS > 24 || B > NW) return false;
+  if (NW == 4) return B == 1 || B == 2;
   if (NW == 8) return B == 1 || B == 2 || B == 3 || B == 4;
   if (NW == 16) return B == 1 || B == 2 || B == 4 || B == 6 || B == 8;
   return false;
@@ -862,7 +863,10 @@ bool shape_supported(int B, int NW, int KS) {
 // pick (B rows per batch, NW warps per CTA): an explicit request must fit; auto prefers 8-warp CTAs with
 // three (then two) resident per SM -- barrier and latency stalls of one overlap the others -- then one
 // 16-warp CTA, largest B first.
-bool pick_shape(int T, int k, int req_B, int req_NW, Shape* out) {
+// heads: the index has head features (-1 unknown).  Without them there is little cross-row reuse and short
+// slices, so small CTAs (4 warps, one row, 4-6 per SM) that barrier rarely and overlap well win; with them
+// (Zipf-like S) batches of rows share slices and head tables, and three 8-warp CTAs per SM win.
+bool pick_shape(int T, int k, int req_B, int req_NW, int heads, Shape* out) {
   const int KS = ks_for_k(k);
   const size_t max_smem = 227 * 1024;
   const size_t per_sm = 228 * 1024;
@@ -874,7 +878,7 @@ bool pick_shape(int T, int k, int req_B, int req_NW, Shape* out) {
   };
   const int Bs[] = {8, 6, 4, 3, 2, 1};
   if (req_B || req_NW) {
-    for (int NW : {8, 16}) {
+    for (int NW : {8, 16, 4}) {
       if (req_NW && NW != req_NW) continue;
       for (int B : Bs) {
         if (req_B && B != req_B) continue;
@@ -883,6 +887,9 @@ bool pick_shape(int T, int k, int req_B, int req_NW, Shape* out) {
     }
     return false;
   }
+  if (heads == 0)
+    for (int ctas : {6, 5, 4})
+      if (fits(1, 4, ctas)) { *out = {1, 4}; return true; }
   for (int B : Bs)
     if (B >= 2 && fits(B, 8, 3)) { *out = {B, 8}; return true; }
   for (int B : Bs)
@@ -944,7 +951,12 @@ cudaError_t launch_ks(const QP& p, int sms, cudaStream_t st) {
 }
 
 cudaError_t launch_shape(const Shape& sh, const QP& p, int sms, cudaStream_t st) {
-  if (sh.NW == 8) {
+  if (sh.NW == 4) {
+    switch (sh.B) {
+      case 1: return launch_ks<1, 4>(p, sms, st);
+      case 2: return launch_ks<2, 4>(p, sms, st);
+    }
+  } else if (sh.NW == 8) {
     switch (sh.B) {
       case 1: return launch_ks<1, 8>(p, sms, st);
       case 2: return launch_ks<2, 8>(p, sms, st);
@@ -989,14 +1001,19 @@ using namespace kj;
 KJ_API size_t knnjoin_query_workspace_bytes(const knnjoin_index* idx, const knnjoin_csr* R, int32_t k,
                                             const knnjoin_query_options* qopt) {
   if (!check_query_args(idx, R, k)) return 0;
-  Shape sh;
-  if (!pick_shape(idx->tile, k, qopt ? qopt->batch_rows : 0, qopt ? qopt->cta_warps : 0, &sh)) {
-    set_error("no (batch_rows, cta_warps) shape fits shared memory for tile %d, k %d", idx->tile, k);
-    return 0;
+  // the auto shape may depend on the index's head count (known on the device): size for both candidates
+  size_t best = 0;
+  for (int heads : {0, 1}) {
+    Shape sh;
+    if (!pick_shape(idx->tile, k, qopt ? qopt->batch_rows : 0, qopt ? qopt->cta_warps : 0, heads, &sh)) {
+      set_error("no (batch_rows, cta_warps) shape fits shared memory for tile %d, k %d", idx->tile, k);
+      return 0;
+    }
+    QueryWs W;
+    query_ws_layout(R->n_rows, R->nnz, sh.B, k, &W);
+    if (W.total > best) best = W.total;
   }
-  QueryWs W;
-  query_ws_layout(R->n_rows, R->nnz, sh.B, k, &W);
-  return W.total;
+  return best;
 }
 
 KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr* R, int32_t k,
@@ -1010,8 +1027,19 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
     set_error("integer scores may overflow 32 bits for d = %d", idx->d);
     return KNNJOIN_ERR_UNSUPPORTED;
   }
+  const bool auto_shape = !qopt || (qopt->batch_rows == 0 && qopt->cta_warps == 0);
+  if (auto_shape && idx->n_head_host < 0) {
+    // first auto-shaped query on this index: read its head count once (4-byte copy; synchronises `stream`)
+    int32_t nh = 0;
+    cudaError_t e0 = cudaMemcpyAsync(&nh, idx->head_feat + kMaxHead, sizeof(nh), cudaMemcpyDeviceToHost,
+                                     (cudaStream_t)stream);
+    if (e0 == cudaSuccess) e0 = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e0 != cudaSuccess) return cuda_fail(e0, "read head count");
+    idx->n_head_host = nh;
+  }
   Shape sh;
-  if (!pick_shape(idx->tile, k, qopt ? qopt->batch_rows : 0, qopt ? qopt->cta_warps : 0, &sh)) {
+  if (!pick_shape(idx->tile, k, qopt ? qopt->batch_rows : 0, qopt ? qopt->cta_warps : 0,
+                  idx->n_head_host < 0 ? 1 : (idx->n_head_host > 0 ? 1 : 0), &sh)) {
     set_error("batch_rows %d / cta_warps %d unsupported for tile %d, k %d", qopt ? qopt->batch_rows : 0,
               qopt ? qopt->cta_warps : 0, idx->tile, k);
     return KNNJOIN_ERR_UNSUPPORTED;
