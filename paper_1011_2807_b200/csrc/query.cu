@@ -789,29 +789,52 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
         for (int s = 0; s < KS; ++s)
           if (s * 32 + lane < k) scratch[((size_t)warp * B + b) * k + s * 32 + lane] = L[b][s];
       __syncthreads();
-      if (warp < nb) {
-        uint64_t M[KS];
-#pragma unroll
-        for (int s = 0; s < KS; ++s) M[s] = 0;
-        uint64_t th = kKeyFloor;
-        for (int w = 0; w < NW; ++w) {
-#pragma unroll
-          for (int s = 0; s < KS; ++s) {
-            const int pos = s * 32 + lane;
-            uint64_t c = pos < k ? scratch[((size_t)w * B + warp) * k + pos] : 0;
-            list_offer_lanes<KS>(M, c, th, k, lane);
-          }
+      // The NW lists of a row are sorted and hold distinct keys (distinct columns), so the merged position
+      // of a key is its position in its own list plus the number of larger keys in the other lists (binary
+      // searches): every thread places keys independently.  Positions past the row's positive keys are
+      // padding (reading c2).
+      auto emit = [&](int b, int pos, uint64_t key) {
+        const int64_t r = row0 + b;
+        const size_t o = (size_t)r * k + pos;
+        if (!last_pass) {
+          __stcg((unsigned long long*)p.state_keys + o, (unsigned long long)key);
+          return;
         }
-        const int64_t r = row0 + warp;
-        if (last_pass) {
-          list_finalize<KS>(M, k, r, p.inv_sigma[r], p.out_keys, p.out_ids, p.out_scores, lane);
+        const uint32_t score = (uint32_t)(key >> 32);
+        if (score == 0) {
+          if (p.out_keys) p.out_keys[o] = 0;
+          if (p.out_ids) p.out_ids[o] = -1;
+          if (p.out_scores) p.out_scores[o] = 0.0f;
         } else {
-#pragma unroll
-          for (int s = 0; s < KS; ++s) {
-            const int pos = s * 32 + lane;
-            if (pos < k) __stcg((unsigned long long*)p.state_keys + (size_t)r * k + pos, (unsigned long long)M[s]);
-          }
+          if (p.out_keys) p.out_keys[o] = key;
+          if (p.out_ids) p.out_ids[o] = (int32_t)(0xFFFFFFFFu - (uint32_t)key);
+          if (p.out_scores) p.out_scores[o] = (float)((double)score * p.inv_sigma[r]);
         }
+      };
+      auto count_gt = [&](const uint64_t* lst, uint64_t x) {  // keys > x in a descending list of k
+        int lo = 0, hi = k;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (lst[mid] > x) lo = mid + 1; else hi = mid;
+        }
+        return lo;
+      };
+      for (int i = tid; i < NW * B * k; i += NT_) {
+        const int w = i / (B * k), b = (i / k) % B, pos = i % k;
+        if (b >= nb) continue;
+        const uint64_t x = scratch[i];
+        if (x == 0) continue;
+        int rank = pos;
+        for (int w2 = 0; w2 < NW && rank < k; ++w2)
+          if (w2 != w) rank += count_gt(scratch + ((size_t)w2 * B + b) * k, x);
+        if (rank < k) emit(b, rank, x);
+      }
+      for (int i = tid; i < B * k; i += NT_) {
+        const int b = i / k, pos = i % k;
+        if (b >= nb) continue;
+        int npos = 0;
+        for (int w = 0; w < NW && npos <= pos; ++w) npos += count_gt(scratch + ((size_t)w * B + b) * k, 0);
+        if (pos >= npos) emit(b, pos, 0);
       }
       __syncthreads();
       if (!last_pass && tid == 0) {
