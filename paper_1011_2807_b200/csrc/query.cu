@@ -64,16 +64,26 @@ struct QP {
   float* out_scores;
 };
 
-__device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
+// Posting loads skip L1 (no reuse inside an SM) but must stay in L2 at normal priority: the slab of S tiles of
+// the current pass is re-read by every batch.  (A bare L1::no_allocate load is issued as L2 evict-first on
+// sm_100a -- ncu showed 80 % of C5's index sectors missing L2 -- so the L2 policy is given explicitly.)
+__device__ __forceinline__ uint64_t l2_policy_normal() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint4 ldg_nc_v4(const void* p, uint64_t pol) {
   uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
+               : "l"(p), "l"(pol));
   return r;
 }
-__device__ __forceinline__ uint2 ldg_nc_v2(const void* p) {
+__device__ __forceinline__ uint2 ldg_nc_v2(const void* p, uint64_t pol) {
   uint2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+               : "=r"(r.x), "=r"(r.y)
+               : "l"(p), "l"(pol));
   return r;
 }
 
@@ -361,6 +371,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
     }
   };
   unsigned long long n_visits = 0, n_inserts = 0, n_complete = 0, n_skipped = 0;
+  const uint64_t l2pol = l2_policy_normal();
   const int n_head = p.head_feat[kMaxHead];
   const int n_groups = (n_head + 3) >> 2;
 
@@ -558,8 +569,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
             uint4 idA = make_uint4(0, 0, 0, 0);
             uint2 wA = make_uint2(0, 0);
             if (vA) {
-              idA = ldg_nc_v4(p.ids + (size_t)uA * 8);
-              if (wint8) wA = ldg_nc_v2(p.vals + (size_t)uA * 8);
+              idA = ldg_nc_v4(p.ids + (size_t)uA * 8, l2pol);
+              if (wint8) wA = ldg_nc_v2(p.vals + (size_t)uA * 8, l2pol);
             }
             for (uint32_t p0 = p_begin; p0 < p_end; p0 += 32) {
               int eB = 0;
@@ -570,8 +581,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
               if (p0 + 32 < p_end) {
                 lookup(p0 + 32, eB, uB, vB);
                 if (vB) {
-                  idB = ldg_nc_v4(p.ids + (size_t)uB * 8);
-                  if (wint8) wB = ldg_nc_v2(p.vals + (size_t)uB * 8);
+                  idB = ldg_nc_v4(p.ids + (size_t)uB * 8, l2pol);
+                  if (wint8) wB = ldg_nc_v2(p.vals + (size_t)uB * 8, l2pol);
                 }
               }
               if (vA) {
