@@ -26,9 +26,8 @@
 //   5. k_units: units(key) = ceil(count/8) (0 for head features); CUB exclusive scan: off = scan(units)
 //   6. k_fill_pads, k_scatter (posting of sorted rank rho at position rho of its slice), k_block_layout:
 //      inside every full 256-posting block (32 units) the postings are ordered by shared-memory bank
-//      (id mod 32), so slot j of the 32 units holds postings of ~32 distinct banks; the final partial block
-//      of m units is transposed (unit i holds sorted postings i, i+m, ..., i+7m) so the lanes of a warp hit
-//      consecutive ids
+//      (id mod 32), so slot j of the units holds postings of ~distinct banks; the final partial block of
+//      m units gets the same bank order
 //   7. k_head_cols: one 32-bit head word per S row.
 // The paper counts this as Eq. 4's first term, sum |s_i| postings.
 #include <cub/cub.cuh>
@@ -248,9 +247,8 @@ __global__ void k_scatter(const uint32_t* __restrict__ keys, const uint32_t* __r
   if (wvals) wvals[pos] = (uint8_t)(v >> 16);
 }
 
-// Warp per slice (grid-stride over keys).  Full 256-posting blocks: stable counting sort by bank
-// (id mod 32; padding last): rank r -> position r (unit r/8, slot r%8).  Final partial block of m units:
-// transpose (unit i holds sorted postings i, i+m, ...).  Deterministic: ranks come from slot-ordered
+// Warp per slice (grid-stride over keys).  Every block of m <= 32 units (256 postings when full): stable
+// counting sort by bank (id mod 32; padding last): rank r -> position r (unit r/8, slot r%8).  Deterministic: ranks come from slot-ordered
 // match_any passes, not from the order of atomics.
 __global__ void k_block_layout(const uint32_t* __restrict__ off, const uint32_t* __restrict__ units, int64_t n_keys,
                                uint32_t tile, uint16_t* __restrict__ ids, uint8_t* __restrict__ wvals) {
@@ -282,16 +280,21 @@ __global__ void k_block_layout(const uint32_t* __restrict__ off, const uint32_t*
           for (int j = 0; j < 8; ++j) w[j] = (uint8_t)((j < 4 ? y.x : y.y) >> (8 * (j & 3)));
         }
       }
+      // stable counting sort by bank (bucket 32 = padding, after every real posting; bucket 33 = lanes past
+      // the block's m units, not counted): rank r -> unit r / 8, slot r % 8.  Slot j of the m units then
+      // holds ranks j, 8 + j, ..., i.e. postings spread across the bank order: ~distinct banks per warp
+      // instruction for sparse slices, consecutive banks for dense ones.
       uint32_t dst[8];
-      if (m == 32) {
+      {
         cnt[lane] = 0;
         if (lane == 0) cnt[32] = 0;
         __syncwarp();
+        const bool live = lane < (int)m;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {  // bucket sizes (bucket 32 = padding)
-          const uint32_t bk = id[j] >= tile ? 32u : (id[j] & 31u);
+        for (int j = 0; j < 8; ++j) {  // bucket sizes
+          const uint32_t bk = !live ? 33u : (id[j] >= tile ? 32u : (id[j] & 31u));
           const uint32_t peers = __match_any_sync(0xffffffffu, bk);
-          if ((peers & lt) == 0) cnt[bk] += __popc(peers);
+          if (bk < 33u && (peers & lt) == 0) cnt[bk] += __popc(peers);
           __syncwarp();
         }
         const uint32_t c = cnt[lane];
@@ -307,19 +310,13 @@ __global__ void k_block_layout(const uint32_t* __restrict__ off, const uint32_t*
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < 8; ++j) {  // ranks in (slot, lane) order within each bucket
-          const uint32_t bk = id[j] >= tile ? 32u : (id[j] & 31u);
+          const uint32_t bk = !live ? 33u : (id[j] >= tile ? 32u : (id[j] & 31u));
           const uint32_t peers = __match_any_sync(0xffffffffu, bk);
-          const uint32_t start = cnt[bk];
+          const uint32_t start = bk < 33u ? cnt[bk] : 0u;
           dst[j] = start + __popc(peers & lt);
           __syncwarp();
-          if ((peers & lt) == 0) cnt[bk] = start + __popc(peers);
+          if (bk < 33u && (peers & lt) == 0) cnt[bk] = start + __popc(peers);
           __syncwarp();
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {  // plain position p = 8*lane + j -> unit p % m, slot p / m
-          const uint32_t p = 8u * lane + j;
-          dst[j] = (p % m) * 8 + p / m;
         }
       }
       __syncwarp();

@@ -326,11 +326,12 @@ __host__ __device__ inline size_t smem_bytes(int B, int T, int k, int NW) {
          (size_t)NW * 32 * 4 /* completion queues */ + 32 /* misc */;
 }
 
+constexpr int kWinChunk = 8;  // 32-unit windows a warp takes per grab of the dynamic window counter (B > 1)
+
 __device__ __forceinline__ void red_add_shared(uint32_t addr, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
-constexpr int kWinChunk = 8;  // 32-unit windows a warp takes per grab of the dynamic window counter
 
 template <int B, int KS, bool SINT8, int NW>
 __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_accumulate_topk(QP p) {
@@ -529,21 +530,45 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
           const int n_items = s_misc[1];
           const uint32_t TOT = (uint32_t)s_misc[2];
           const uint32_t nwin = (TOT + 31) >> 5;
-          for (;;) {
-            uint32_t c = 0;
-            if (lane == 0) c = atomicAdd((unsigned*)&s_misc[3], (unsigned)kWinChunk);
-            c = __shfl_sync(0xffffffffu, c, 0);
-            if (c >= nwin) break;
-            const uint32_t p_begin = c * 32, p_end = min(TOT, (c + kWinChunk) * 32);
+          // One row per batch (B == 1, every window costs the same): warp w takes the contiguous windows
+          // [nwin*w/NW, nwin*(w+1)/NW) -- balanced to one window, one binary search per warp, one continuous
+          // load pipeline.  Several rows: a window costs one atomic per posting per row of its run, so warps
+          // grab kWinChunk windows at a time from a shared counter.
+          for (int grab = 0;; ++grab) {
+            uint32_t w0, w1;
+            if (B == 1) {
+              if (grab) break;
+              w0 = (uint32_t)(((uint64_t)nwin * warp) / NW);
+              w1 = (uint32_t)(((uint64_t)nwin * (warp + 1)) / NW);
+              if (w0 >= w1) break;
+            } else {
+              uint32_t c = 0;
+              if (lane == 0) c = atomicAdd((unsigned*)&s_misc[3], (unsigned)kWinChunk);
+              c = __shfl_sync(0xffffffffu, c, 0);
+              if (c >= nwin) break;
+              w0 = c;
+              w1 = min(nwin, c + kWinChunk);
+            }
+            const uint32_t p_begin = w0 * 32, p_end = min(TOT, w1 * 32);
             int lo = 0, hi = n_items - 1;  // largest e with P[e] <= p_begin
             while (lo < hi) {
               int mid = (lo + hi + 1) >> 1;
               if (s_P[mid] <= p_begin) lo = mid; else hi = mid - 1;
             }
             int e_cur = lo;
+            struct Stage {
+              uint4 id;
+              uint2 w;
+              int e;
+              bool v;
+            };
             // lane l takes unit p0 + l.  e_cur is the item covering p0; the items starting inside the window
             // are found with one OR-reduction of their start offsets (starts are strictly increasing).
-            auto lookup = [&](uint32_t p0, int& e_out, uint32_t& unit, bool& valid) {
+            // Windows must be fetched in ascending order (e_cur advances).
+            auto fetch = [&](Stage& S, uint32_t p0) {
+              S.v = false;
+              S.e = e_cur;
+              if (p0 >= p_end) return;
               const uint32_t nxt = s_P[e_cur + 1];
               int e = e_cur, e_next;
               if (p0 + 32 > nxt) {
@@ -556,63 +581,62 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
                 e_next = e_cur + (nxt == p0 + 32 ? 1 : 0);
               }
               const uint32_t pp = p0 + lane;
-              valid = pp < p_end;
-              if (!valid) e = e_cur;
-              e_out = e;
-              unit = s_ustart[e] + (pp - s_P[e]);
+              S.v = pp < p_end;
+              if (!S.v) e = e_cur;
+              S.e = e;
               e_cur = min(e_next, n_items - 1);
+              if (S.v) {
+                const uint32_t unit = s_ustart[e] + (pp - s_P[e]);
+                S.id = ldg_nc_v4(p.ids + (size_t)unit * 8, l2pol);
+                if (wint8) S.w = ldg_nc_v2(p.vals + (size_t)unit * 8, l2pol);
+              }
             };
-            int eA;
-            uint32_t uA;
-            bool vA;
-            lookup(p_begin, eA, uA, vA);
-            uint4 idA = make_uint4(0, 0, 0, 0);
-            uint2 wA = make_uint2(0, 0);
-            if (vA) {
-              idA = ldg_nc_v4(p.ids + (size_t)uA * 8, l2pol);
-              if (wint8) wA = ldg_nc_v2(p.vals + (size_t)uA * 8, l2pol);
-            }
-            for (uint32_t p0 = p_begin; p0 < p_end; p0 += 32) {
-              int eB = 0;
-              uint32_t uB = 0;
-              bool vB = false;
-              uint4 idB = make_uint4(0, 0, 0, 0);
-              uint2 wB = make_uint2(0, 0);
-              if (p0 + 32 < p_end) {
-                lookup(p0 + 32, eB, uB, vB);
-                if (vB) {
-                  idB = ldg_nc_v4(p.ids + (size_t)uB * 8, l2pol);
-                  if (wint8) wB = ldg_nc_v2(p.vals + (size_t)uB * 8, l2pol);
+            auto process = [&](const Stage& S) {
+              if (!S.v) return;
+              const uint32_t mask = s_fm[S.e] >> 24;
+              const uint32_t wd[4] = {S.id.x, S.id.y, S.id.z, S.id.w};
+              uint32_t off4[8], w8[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                off4[j] = ((wd[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu) * 4u;
+                w8[j] = wint8 ? (((j < 4 ? S.w.x : S.w.y) >> (8 * (j & 3))) & 0xFFu) : 1u;
+              }
+#pragma unroll
+              for (int b = 0; b < B; ++b) {
+                if (mask & (1u << b)) {
+                  const uint32_t q = (uint32_t)s_q[S.e * QS + b];
+                  const uint32_t rb = acc_s + (uint32_t)(b * TS * 4);
+#pragma unroll
+                  for (int j = 0; j < 8; ++j) red_add_shared(rb + off4[j], wint8 ? q * w8[j] : q);
                 }
               }
-              if (vA) {
-                const uint32_t mask = s_fm[eA] >> 24;
-                const uint32_t wd[4] = {idA.x, idA.y, idA.z, idA.w};
-                uint32_t off4[8], w8[8];
+              if (p.counters) {
+                int nid = 0;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                  off4[j] = ((wd[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu) * 4u;
-                  w8[j] = wint8 ? (((j < 4 ? wA.x : wA.y) >> (8 * (j & 3))) & 0xFFu) : 1u;
-                }
-#pragma unroll
-                for (int b = 0; b < B; ++b) {
-                  if (mask & (1u << b)) {
-                    const uint32_t q = (uint32_t)s_q[eA * QS + b];
-                    const uint32_t rb = acc_s + (uint32_t)(b * TS * 4);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                      red_add_shared(rb + off4[j], wint8 ? q * w8[j] : q);
-                    }
-                  }
-                }
-                if (p.counters) {
-                  int nid = 0;
-#pragma unroll
-                  for (int j = 0; j < 8; ++j) nid += off4[j] < (uint32_t)T * 4u;
-                  n_visits += (unsigned long long)nid * __popc(mask);
-                }
+                for (int j = 0; j < 8; ++j) nid += off4[j] < (uint32_t)T * 4u;
+                n_visits += (unsigned long long)nid * __popc(mask);
               }
-              eA = eB; uA = uB; vA = vB; idA = idB; wA = wB;
+            };
+            Stage A, Bs, C;
+            A.id = Bs.id = C.id = make_uint4(0, 0, 0, 0);
+            A.w = Bs.w = C.w = make_uint2(0, 0);
+            fetch(A, p_begin);
+            if constexpr (B == 1) {  // two windows in flight (registers are plentiful at one row)
+              fetch(Bs, p_begin + 32);
+              for (uint32_t p0 = p_begin; p0 < p_end; p0 += 96) {
+                fetch(C, p0 + 64);
+                process(A);
+                fetch(A, p0 + 96);
+                process(Bs);
+                fetch(Bs, p0 + 128);
+                process(C);
+              }
+            } else {  // one window in flight
+              for (uint32_t p0 = p_begin; p0 < p_end; p0 += 32) {
+                fetch(Bs, p0 + 32);
+                process(A);
+                A = Bs;
+              }
             }
           }
           __syncthreads();
