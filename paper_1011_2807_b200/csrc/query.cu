@@ -42,6 +42,7 @@ struct QP {
   int32_t d, T;
   int64_t NT;
   int64_t s_id_base;
+  int32_t head_smem;         // shared memory holds head tables (0 only when the index has no head features)
   // R / batches
   int64_t n_r;
   int32_t k;
@@ -315,15 +316,17 @@ __host__ __device__ inline size_t head_at(int B, int T, int k, int NW) {
   return align_up(staging_at(B, T, k, NW) + (size_t)kcap(NW) * B * 4 + (size_t)kcap(NW) * 8 +
                       (size_t)(kcap(NW) + 1) * 4, 16);
 }
-__host__ __device__ inline size_t head_bytes(int B) {
-  return (size_t)(kMaxHead / 4) * B * 16 * 4 + (size_t)B * (kMaxHead + 1) * 4 + (size_t)B * 4;
+// (heads = false: the index has no head features; the head tables and completion queues are left out so that
+// six one-row CTAs fit on an SM)
+__host__ __device__ inline size_t head_bytes(int B, bool heads) {
+  return heads ? (size_t)(kMaxHead / 4) * B * 16 * 4 + (size_t)B * (kMaxHead + 1) * 4 + (size_t)B * 4 : 0;
 }
-__host__ __device__ inline size_t tail_at(int B, int T, int k, int NW) {
-  return align_up(head_at(B, T, k, NW) + head_bytes(B), 16);
+__host__ __device__ inline size_t tail_at(int B, int T, int k, int NW, bool heads) {
+  return align_up(head_at(B, T, k, NW) + head_bytes(B, heads), 16);
 }
-__host__ __device__ inline size_t smem_bytes(int B, int T, int k, int NW) {
-  return tail_at(B, T, k, NW) + (size_t)NW * 8 /* scan partials */ + (size_t)B * 8 /* theta */ +
-         (size_t)NW * 32 * 4 /* completion queues */ + 32 /* misc */;
+__host__ __device__ inline size_t smem_bytes(int B, int T, int k, int NW, bool heads) {
+  return tail_at(B, T, k, NW, heads) + (size_t)NW * 8 /* scan partials */ + (size_t)B * 8 /* theta */ +
+         32 /* misc */ + (heads ? (size_t)NW * 32 * 4 : 0) /* completion queues */;
 }
 
 constexpr int kWinChunk = 8;  // 32-unit windows a warp takes per grab of the dynamic window counter (B > 1)
@@ -353,12 +356,12 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
   uint32_t* s_hmask = s_cum + B * (kMaxHead + 1);                    // [B]
   int32_t* s_qh = s_q;                                                // [kMaxHead][B], aliases staging
   static_assert(kMaxHead * B <= kcap(NW) * B, "q_head must fit in the staging area");
-  uint64_t* s_warp = (uint64_t*)(smem + tail_at(B, T, p.k, NW));
+  uint64_t* s_warp = (uint64_t*)(smem + tail_at(B, T, p.k, NW, p.head_smem));
   uint64_t* s_theta = s_warp + NW;           // [B]: max over warps of their k-th key per row
-  int* s_misc = (int*)((uint32_t*)(s_theta + B) + NW * 32);  // [0] batch, [1] n sparse items, [2] TOT, [3] window counter
+  int* s_misc = (int*)(s_theta + B);         // [0] batch, [1] n sparse items, [2] TOT, [3] window counter
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint32_t* s_queue = (uint32_t*)(s_theta + B) + warp * 32;  // this warp's head-completion queue
+  uint32_t* s_queue = (uint32_t*)(s_misc + 8) + warp * 32;  // this warp's head-completion queue (heads only)
   const int k = p.k;
   constexpr bool wint8 = SINT8;
   const bool timing = p.phase != nullptr && tid == 0;
@@ -373,7 +376,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
   };
   unsigned long long n_visits = 0, n_inserts = 0, n_complete = 0, n_skipped = 0;
   const uint64_t l2pol = l2_policy_normal();
-  const int n_head = p.head_feat[kMaxHead];
+  const int n_head = p.head_smem ? p.head_feat[kMaxHead] : 0;  // host guarantees head_smem when n_head > 0
   const int n_groups = (n_head + 3) >> 2;
 
   for (int i = tid; i < (int)(acc_region_bytes(B, T, k, NW) / 16); i += NT_) ((uint4*)acc)[i] = make_uint4(0, 0, 0, 0);
@@ -931,7 +934,7 @@ bool pick_shape(int T, int k, int req_B, int req_NW, int heads, Shape* out) {
   auto fits = [&](int B, int NW, int ctas) {
     if (!shape_supported(B, NW, KS)) return false;
     if (T % (NW * 128) != 0) return false;
-    size_t b = smem_bytes(B, T, k, NW);
+    size_t b = smem_bytes(B, T, k, NW, heads != 0);
     return b <= max_smem && ctas * (b + 1024) <= per_sm;
   };
   const int Bs[] = {8, 6, 4, 3, 2, 1};
@@ -976,7 +979,7 @@ bool query_ws_layout(int64_t n_r, int64_t nnz_r, int B, int k, QueryWs* W) {
 
 template <int B, int KS, bool SINT8, int NW>
 cudaError_t launch_main4(const QP& p, int sms, cudaStream_t st) {
-  const size_t sm = smem_bytes(B, p.T, p.k, NW);
+  const size_t sm = smem_bytes(B, p.T, p.k, NW, p.head_smem != 0);
   auto kern = k_accumulate_topk<B, KS, SINT8, NW>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
@@ -1158,6 +1161,7 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
   p.T = idx->tile;
   p.NT = idx->n_tiles;
   p.s_id_base = idx->s_id_base;
+  p.head_smem = idx->n_head_host != 0 ? 1 : 0;  // -1 (unknown) keeps the head tables
   p.n_r = R->n_rows;
   p.k = k;
   p.n_batches = n_batches;
