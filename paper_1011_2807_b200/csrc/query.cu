@@ -329,6 +329,15 @@ __host__ __device__ inline size_t smem_bytes(int B, int T, int k, int NW, bool h
          32 /* misc */ + (heads ? (size_t)NW * 32 * 4 : 0) /* completion queues */;
 }
 
+__device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(addr) : "memory");
+  return r;
+}
+__device__ __forceinline__ void sts_v4_zero(uint32_t addr) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(addr), "r"(0u) : "memory");
+}
+
 constexpr int kWinChunk = 8;  // 32-unit windows a warp takes per grab of the dynamic window counter (B > 1)
 
 __device__ __forceinline__ void red_add_shared(uint32_t addr, uint32_t v) {
@@ -682,6 +691,40 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
         uint64_t th[B];
 #pragma unroll
         for (int b = 0; b < B; ++b) th[b] = row_theta(b);
+        if (n_groups == 0) {
+          // no head features: the accumulated score is the score.  Per 128-column step a lane reads 4 scores
+          // of each row (32-bit shared addresses), zero-fills, and only a warp with a score >= theta's score
+          // leaves the fast loop to offer its keys.
+          uint32_t t32[B];
+#pragma unroll
+          for (int b = 0; b < B; ++b) t32[b] = t32_of(th[b]);
+          const uint32_t a0 = acc_s + (uint32_t)(cbase + lane * 4) * 4u;
+#pragma unroll 2
+          for (int c = 0; c < cols; c += 128) {
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+              if (b < nb) {
+                const uint32_t a = a0 + (uint32_t)(b * TS + c) * 4u;
+                const uint4 x = lds_v4(a);
+                sts_v4_zero(a);
+                const uint32_t mx = max(max(x.x, x.y), max(x.z, x.w));
+                if (__any_sync(0xffffffffu, mx >= t32[b])) {
+                  th[b] = row_theta(b);
+                  const uint32_t g0 = gbase + (uint32_t)(cbase + c + lane * 4);
+                  const uint32_t xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) {
+                    const uint64_t key = xv[j] ? make_key(xv[j], g0 + j) : 0;
+                    const int n = list_offer_lanes<KS>(L[b], key, th[b], k, lane);  // warp-collective
+                    n_inserts += (lane == 0) ? n : 0;
+                  }
+                  publish(b);
+                  t32[b] = t32_of(th[b]);
+                }
+              }
+            }
+          }
+        } else
         for (int c = 0; c < cols; c += 128) {
           const int col = cbase + c + lane * 4;
           const uint32_t g0 = gbase + (uint32_t)col;
