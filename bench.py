@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--batch-rows", type=int, default=0)
     ap.add_argument("--cta-warps", type=int, default=0)
     ap.add_argument("--tiles-per-pass", type=int, default=0)
+    ap.add_argument("--row-order", type=int, default=0, help="0 work-sorted (a3), 1 input order")
     ap.add_argument("--head-density", type=float, default=0.0, help="0 auto (1/8), <0 no head features")
     ap.add_argument("--head-max", type=int, default=0, help="0 auto (64)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -248,10 +249,10 @@ def bench_ours(args):
             build_event.record(stream)
         if world == 1:
             ids, sc, _ = kj.knnjoin_query(idx, dR_, k, batch_rows=args.batch_rows, events=kernel_events,
-                                          cta_warps=args.cta_warps, tiles_per_pass=args.tiles_per_pass)
+                                          cta_warps=args.cta_warps, tiles_per_pass=args.tiles_per_pass, row_order=args.row_order)
             return ids, sc
         _, _, keys = kj.knnjoin_query(idx, dR_, k, want_keys=True, want_ids=False, batch_rows=args.batch_rows,
-                                      events=kernel_events, cta_warps=args.cta_warps, tiles_per_pass=args.tiles_per_pass)
+                                      events=kernel_events, cta_warps=args.cta_warps, tiles_per_pass=args.tiles_per_pass, row_order=args.row_order)
         gathered = kdist.all_gather_keys(keys)  # one NCCL all_gather_into_tensor over NVLink
         ids, sc, _ = kj.knnjoin_merge(gathered, dR_, d, dS_.dtype, k)
         return ids, sc
@@ -276,13 +277,13 @@ def bench_ours(args):
     # per-phase SM cycles of the accumulate kernel (one untimed instrumented step)
     phase = torch.zeros(8, dtype=torch.int64, device=dev)
     idx_p = kj.knnjoin_build_index(dS, d, s_id_base=s_base, tile=args.tile, head_density=args.head_density, head_max=args.head_max)
-    kj.knnjoin_query(idx_p, dR, k, batch_rows=args.batch_rows, phase_cycles=phase, cta_warps=args.cta_warps, tiles_per_pass=args.tiles_per_pass)
+    kj.knnjoin_query(idx_p, dR, k, batch_rows=args.batch_rows, phase_cycles=phase, cta_warps=args.cta_warps, tiles_per_pass=args.tiles_per_pass, row_order=args.row_order)
     torch.cuda.synchronize()
     ph = phase.cpu().tolist()
     cnt = torch.zeros(4, dtype=torch.int64, device=dev)
     idx_c = kj.knnjoin_build_index(dS, d, s_id_base=s_base, tile=args.tile, head_density=args.head_density,
                                    head_max=args.head_max)
-    kj.knnjoin_query(idx_c, dR, k, batch_rows=args.batch_rows, counters=cnt, cta_warps=args.cta_warps, tiles_per_pass=args.tiles_per_pass)
+    kj.knnjoin_query(idx_c, dR, k, batch_rows=args.batch_rows, counters=cnt, cta_warps=args.cta_warps, tiles_per_pass=args.tiles_per_pass, row_order=args.row_order)
     torch.cuda.synchronize()
     counters = dict(zip(["postings_visited", "inserts", "head_postings_skipped", "head_completions"],
                         cnt.cpu().tolist()))

@@ -38,7 +38,7 @@ class _Options(ctypes.Structure):
 class _QueryOptions(ctypes.Structure):
     _fields_ = [("batch_rows", ctypes.c_int32), ("counters", ctypes.c_void_p), ("ev_begin", ctypes.c_void_p),
                 ("ev_end", ctypes.c_void_p), ("phase_cycles", ctypes.c_void_p), ("cta_warps", ctypes.c_int32),
-                ("tiles_per_pass", ctypes.c_int32)]
+                ("tiles_per_pass", ctypes.c_int32), ("row_order", ctypes.c_int32)]
 
 
 class _IndexInfo(ctypes.Structure):
@@ -214,14 +214,15 @@ def knnjoin_index_stats(index: Index) -> dict:
 def knnjoin_query(index: Index, R: DeviceCSR, k: int, want_keys: bool = False, want_ids: bool = True,
                   batch_rows: int = 0, counters: torch.Tensor | None = None, events=None, stream=None,
                   workspace: torch.Tensor | None = None, phase_cycles: torch.Tensor | None = None,
-                  cta_warps: int = 0, tiles_per_pass: int = 0):
+                  cta_warps: int = 0, tiles_per_pass: int = 0, row_order: int = 0):
     """Returns (ids int32 [n,k], scores float32 [n,k], keys uint64-as-int64 [n,k] or None)."""
     cR = R._c()
     if events and (events[0].cuda_event == 0 or events[1].cuda_event == 0):
         raise ValueError("timing events must have been recorded once (so their cudaEvent handles exist)")
     qo = _QueryOptions(batch_rows, counters.data_ptr() if counters is not None else 0,
                        events[0].cuda_event if events else 0, events[1].cuda_event if events else 0,
-                       phase_cycles.data_ptr() if phase_cycles is not None else 0, cta_warps, tiles_per_pass)
+                       phase_cycles.data_ptr() if phase_cycles is not None else 0, cta_warps, tiles_per_pass,
+                       row_order)
     wbytes = _lib.knnjoin_query_workspace_bytes(index.handle, ctypes.byref(cR), k, ctypes.byref(qo))
     if wbytes == 0:
         raise KnnJoinError(1, "knnjoin_query_workspace_bytes", knnjoin_last_error())

@@ -48,6 +48,8 @@ struct QP {
   int32_t k;
   int64_t n_batches;
   const int64_t* r_indptr;
+  const int32_t* perm;      // [n_r] original row of each work-sorted position (nullptr: input order)
+  const int64_t* rbase;     // [n_r] first run slot of each sorted position's row (nullptr: r_indptr)
   const uint32_t* runs_f;
   const int32_t* runs_q;
   const uint32_t* batch_nruns;
@@ -124,18 +126,20 @@ __device__ __forceinline__ int32_t quantize(const void* __restrict__ values, knn
 __device__ void warp_merge_runs(int64_t batch, int lane, const int64_t* __restrict__ indptr,
                                 const int32_t* __restrict__ indices, const void* __restrict__ values,
                                 knnjoin_dtype rdt, int64_t n_r, int32_t d, int B, const double* __restrict__ sigma,
+                                const int32_t* __restrict__ perm, const int64_t* __restrict__ rbase,
                                 uint32_t* __restrict__ runs_f, int32_t* __restrict__ runs_q,
                                 uint32_t* __restrict__ batch_nruns) {
-  int64_t row = batch * B + lane;
-  bool mine = lane < B && row < n_r;
+  const int64_t pos = batch * B + lane;  // position in the (work-sorted) row order
+  bool mine = lane < B && pos < n_r;
   int64_t ptr = 0, end = 0;
   double sg = 1.0;
   if (mine) {
+    const int64_t row = perm ? perm[pos] : pos;
     ptr = indptr[row];
     end = indptr[row + 1];
     sg = sigma[row];
   }
-  int64_t base = indptr[batch * B];
+  int64_t base = rbase ? rbase[batch * B] : indptr[batch * B];
   uint32_t nruns = 0;
   for (;;) {
     int32_t f = 0x7FFFFFFF;
@@ -175,6 +179,8 @@ __global__ void __launch_bounds__(kRunThreads) k_build_runs(const int64_t* __res
                                                             const void* __restrict__ values, knnjoin_dtype rdt,
                                                             int64_t n_r, int32_t d, int B, int64_t n_batches,
                                                             const double* __restrict__ sigma,
+                                                            const int32_t* __restrict__ perm,
+                                                            const int64_t* __restrict__ rbase,
                                                             uint32_t* __restrict__ runs_f, int32_t* __restrict__ runs_q,
                                                             uint32_t* __restrict__ batch_nruns) {
   using BRS = cub::BlockRadixSort<uint32_t, kRunThreads, kRunItems, int32_t>;
@@ -188,12 +194,27 @@ __global__ void __launch_bounds__(kRunThreads) k_build_runs(const int64_t* __res
   const int64_t batch = blockIdx.x;
   if (batch >= n_batches) return;
   const int tid = threadIdx.x;
-  const int64_t row0 = batch * B;
-  const int64_t rowN = min(n_r, row0 + B);
-  const int64_t e0 = indptr[row0], e1 = indptr[rowN];
-  const int64_t ne = e1 - e0;
+  const int64_t pos0 = batch * B;  // batch rows are positions pos0.. of the (work-sorted) row order
+  const int nb = (int)min((int64_t)B, n_r - pos0);
+  // entry j of the batch (rows concatenated in batch order) lives at CSR position rs[b] + (j - pre[b])
+  int64_t rs[8], pre[9];
+  pre[0] = 0;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    rs[b] = 0;
+    int64_t len = 0;
+    if (b < nb) {
+      const int64_t row = perm ? perm[pos0 + b] : pos0 + b;
+      rs[b] = indptr[row];
+      len = indptr[row + 1] - rs[b];
+    }
+    pre[b + 1] = pre[b] + len;
+  }
+  const int64_t ne = pre[8];
   if (ne > kRunThreads * kRunItems) {
-    if (tid < 32) warp_merge_runs(batch, tid, indptr, indices, values, rdt, n_r, d, B, sigma, runs_f, runs_q, batch_nruns);
+    if (tid < 32)
+      warp_merge_runs(batch, tid, indptr, indices, values, rdt, n_r, d, B, sigma, perm, rbase, runs_f, runs_q,
+                      batch_nruns);
     return;
   }
   // key = feature << 3 | row-in-batch (entries with feature >= d sort last and are dropped)
@@ -201,17 +222,17 @@ __global__ void __launch_bounds__(kRunThreads) k_build_runs(const int64_t* __res
   int32_t q[kRunItems];
 #pragma unroll
   for (int it = 0; it < kRunItems; ++it) {
-    const int64_t e = e0 + tid * kRunItems + it;
+    const int64_t j = tid * kRunItems + it;
     key[it] = 0xFFFFFFFFu;
     q[it] = 0;
-    if (e < e1) {
-      // row of entry e: rows are few (B <= 8), a linear walk over the batch's indptr is enough
+    if (j < ne) {
       int b = 0;
-      while (b + 1 < (int)(rowN - row0) && indptr[row0 + b + 1] <= e) ++b;
+      while (b + 1 < nb && pre[b + 1] <= j) ++b;
+      const int64_t e = rs[b] + (j - pre[b]);
       const int32_t f = indices[e];
       if (f < d) {
         key[it] = ((uint32_t)f << 3) | (uint32_t)b;
-        q[it] = quantize(values, rdt, e, sigma[row0 + b]);
+        q[it] = quantize(values, rdt, e, sigma[perm ? perm[pos0 + b] : pos0 + b]);
       }
     }
   }
@@ -242,7 +263,7 @@ __global__ void __launch_bounds__(kRunThreads) k_build_runs(const int64_t* __res
 #pragma unroll
   for (int it = 0; it < kRunItems; ++it) sm.keys[tid * kRunItems + it] = keys_local[it];
   __syncthreads();
-  const size_t base = (size_t)e0;
+  const size_t base = (size_t)(rbase ? rbase[pos0] : indptr[pos0]);
 #pragma unroll
   for (int it = 0; it < kRunItems; ++it) {
     if (is_start[it]) {
@@ -408,7 +429,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
     const bool last_pass = pass == p.n_passes - 1;
     const int64_t row0 = batch * B;
     const int nb = (int)min((int64_t)B, p.n_r - row0);
-    const int64_t run_base = p.r_indptr[row0];
+    const int64_t run_base = p.rbase ? p.rbase[row0] : p.r_indptr[row0];
     const int nruns = (int)p.batch_nruns[batch];
     if (pass > 0) {
       if (tid == 0) {
@@ -875,12 +896,12 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
       // searches): every thread places keys independently.  Positions past the row's positive keys are
       // padding (reading c2).
       auto emit = [&](int b, int pos, uint64_t key) {
-        const int64_t r = row0 + b;
-        const size_t o = (size_t)r * k + pos;
-        if (!last_pass) {
-          __stcg((unsigned long long*)p.state_keys + o, (unsigned long long)key);
+        if (!last_pass) {  // state is kept per sorted position
+          __stcg((unsigned long long*)p.state_keys + (size_t)(row0 + b) * k + pos, (unsigned long long)key);
           return;
         }
+        const int64_t r = p.perm ? (int64_t)p.perm[row0 + b] : row0 + b;
+        const size_t o = (size_t)r * k + pos;
         const uint32_t score = (uint32_t)(key >> 32);
         if (score == 0) {
           if (p.out_keys) p.out_keys[o] = 0;
@@ -949,7 +970,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
 
 // ------------------------------------------------------------------------------------ host dispatch
 struct QueryWs {
-  size_t sigma_at, inv_at, runs_f_at, runs_q_at, nruns_at, counter_at, state_at, done_at, total;
+  size_t sigma_at, inv_at, runs_f_at, runs_q_at, nruns_at, counter_at, state_at, done_at, wkey_at, wkey2_at,
+      perm_at, perm2_at, rlen_at, rbase_at, cub_at, cub_bytes, total;
 };
 
 struct Shape {
@@ -1016,8 +1038,61 @@ bool query_ws_layout(int64_t n_r, int64_t nnz_r, int B, int k, QueryWs* W) {
   W->counter_at = at; at = align_up(at + 16, 256);
   W->state_at = at;   at = align_up(at + 8 * (size_t)n_r * k, 256);
   W->done_at = at;    at = align_up(at + 4 * (size_t)n_batches, 256);
+  // a3 row order: work keys, permutation (double-buffered for the radix sort), row lengths, run bases
+  size_t sort_bytes = 0, scan_bytes = 0;
+  if (cub::DeviceRadixSort::SortPairsDescending(nullptr, sort_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                                (const int32_t*)nullptr, (int32_t*)nullptr, (int)n_r) != cudaSuccess)
+    return false;
+  if (cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (const int64_t*)nullptr, (int64_t*)nullptr, (int)n_r) !=
+      cudaSuccess)
+    return false;
+  W->cub_bytes = sort_bytes > scan_bytes ? sort_bytes : scan_bytes;
+  W->wkey_at = at;    at = align_up(at + 4 * (size_t)n_r, 256);
+  W->wkey2_at = at;   at = align_up(at + 4 * (size_t)n_r, 256);
+  W->perm_at = at;    at = align_up(at + 4 * (size_t)n_r, 256);
+  W->perm2_at = at;   at = align_up(at + 4 * (size_t)n_r, 256);
+  W->rlen_at = at;    at = align_up(at + 8 * (size_t)n_r, 256);
+  W->rbase_at = at;   at = align_up(at + 8 * (size_t)n_r, 256);
+  W->cub_at = at;     at = align_up(at + W->cub_bytes, 256);
   W->total = at;
   return true;
+}
+
+// a3: per-row work estimate w_r = sum_{d in r} |I_d| (the row's share of Eq. 4's second term),
+// saturated to 32 bits; warp per row.  Sorting rows by w_r (descending) hands the heaviest batches out first
+// so the persistent CTAs finish together.
+__global__ void k_row_work(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices, int64_t n,
+                           int32_t d, const int32_t* __restrict__ df, uint32_t* __restrict__ wkey,
+                           int32_t* __restrict__ iota) {
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  unsigned long long w = 0;
+  for (int64_t j = indptr[row] + lane; j < indptr[row + 1]; j += 32) {
+    const int32_t f = indices[j];
+    if (f < d) w += (unsigned long long)df[f];
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+  if (lane == 0) {
+    // monotone 16-bit code of w (5-bit exponent, 11-bit mantissa): a coarse order needs two radix passes only
+    const uint32_t w32 = w > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)w;
+    uint32_t code = w32;
+    if (w32 >= 2048u) {
+      const uint32_t e = 31u - __clz(w32);  // >= 11
+      code = ((e - 10u) << 11) | ((w32 >> (e - 11u)) & 0x7FFu);
+    }
+    wkey[row] = code;
+    iota[row] = (int32_t)row;
+  }
+}
+
+__global__ void k_sorted_len(const int64_t* __restrict__ indptr, const int32_t* __restrict__ perm, int64_t n,
+                             int64_t* __restrict__ len) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t r = perm[i];
+  len[i] = indptr[r + 1] - indptr[r];
 }
 
 template <int B, int KS, bool SINT8, int NW>
@@ -1175,22 +1250,46 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
   if ((e = cudaMemsetAsync(pass_done, 0, 4 * (size_t)n_batches, st)) != cudaSuccess) return cuda_fail(e, "memset pass_done");
   launch_row_scale(R, idx->d, smax, sigma, inv_sigma, st);
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_row_scale");
+  const int32_t* perm = nullptr;
+  const int64_t* rbase = nullptr;
+  if (!(qopt && qopt->row_order == 1) && R->n_rows > 1) {  // a3: rows by descending work
+    uint32_t* wkey = (uint32_t*)(wb + W.wkey_at);
+    uint32_t* wkey2 = (uint32_t*)(wb + W.wkey2_at);
+    int32_t* iota = (int32_t*)(wb + W.perm_at);
+    int32_t* pm = (int32_t*)(wb + W.perm2_at);
+    int64_t* rlen = (int64_t*)(wb + W.rlen_at);
+    int64_t* rb = (int64_t*)(wb + W.rbase_at);
+    const int64_t n = R->n_rows;
+    k_row_work<<<(unsigned)((n * 32 + 255) / 256), 256, 0, st>>>(R->indptr, R->indices, n, idx->d, idx->df, wkey, iota);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_row_work");
+    size_t cb = W.cub_bytes;
+    if ((e = cub::DeviceRadixSort::SortPairsDescending(wb + W.cub_at, cb, wkey, wkey2, iota, pm, (int)n, 0, 16, st)) !=
+        cudaSuccess)
+      return cuda_fail(e, "row sort");
+    k_sorted_len<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(R->indptr, pm, n, rlen);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_sorted_len");
+    cb = W.cub_bytes;
+    if ((e = cub::DeviceScan::ExclusiveSum(wb + W.cub_at, cb, rlen, rb, (int)n, st)) != cudaSuccess)
+      return cuda_fail(e, "row base scan");
+    perm = pm;
+    rbase = rb;
+  }
   {
     int64_t threads = n_batches * 32;
     // block-sort capacity from the mean entries per batch (x1.5 headroom); larger batches use the warp merge
     const double mean = (double)R->nnz / (double)n_batches * 1.5;
     if (mean <= kRunThreads * 4)
       k_build_runs<4><<<(unsigned)n_batches, kRunThreads, 0, st>>>(R->indptr, R->indices, R->values, R->dtype, R->n_rows,
-                                                                   idx->d, B, n_batches, sigma, runs_f, runs_q, nruns);
+                                                                   idx->d, B, n_batches, sigma, perm, rbase, runs_f, runs_q, nruns);
     else if (mean <= kRunThreads * 8)
       k_build_runs<8><<<(unsigned)n_batches, kRunThreads, 0, st>>>(R->indptr, R->indices, R->values, R->dtype, R->n_rows,
-                                                                   idx->d, B, n_batches, sigma, runs_f, runs_q, nruns);
+                                                                   idx->d, B, n_batches, sigma, perm, rbase, runs_f, runs_q, nruns);
     else if (mean <= kRunThreads * 16)
       k_build_runs<16><<<(unsigned)n_batches, kRunThreads, 0, st>>>(R->indptr, R->indices, R->values, R->dtype, R->n_rows,
-                                                                    idx->d, B, n_batches, sigma, runs_f, runs_q, nruns);
+                                                                    idx->d, B, n_batches, sigma, perm, rbase, runs_f, runs_q, nruns);
     else
       k_build_runs<32><<<(unsigned)n_batches, kRunThreads, 0, st>>>(R->indptr, R->indices, R->values, R->dtype, R->n_rows,
-                                                                    idx->d, B, n_batches, sigma, runs_f, runs_q, nruns);
+                                                                    idx->d, B, n_batches, sigma, perm, rbase, runs_f, runs_q, nruns);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_build_runs");
   }
   QP p;
@@ -1209,6 +1308,8 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
   p.k = k;
   p.n_batches = n_batches;
   p.r_indptr = R->indptr;
+  p.perm = perm;
+  p.rbase = rbase;
   p.runs_f = runs_f;
   p.runs_q = runs_q;
   p.batch_nruns = nruns;

@@ -296,3 +296,16 @@ def test_tile_passes_identical(name, tpp):
     ref = gpu_join(R, S, c.k, tile=2048, tiles_per_pass=1000)
     np.testing.assert_array_equal(ids, ref[0])
     np.testing.assert_array_equal(sc, ref[1])
+
+
+@pytest.mark.parametrize("name,batch_rows,cta_warps", [("C2", 0, 0), ("C2", 3, 8), ("C3", 0, 0), ("C5", 0, 0),
+                                                       ("C1", 8, 16)])
+def test_row_order_identical(name, batch_rows, cta_warps):
+    """a3: batching rows in descending work order (default) == input order, bit for bit, and both match the
+    oracle; ragged last batch (61 rows)."""
+    c = gen.CONFIGS[name].scaled(61, 12000)
+    R, S = gen.generate(c, "R"), gen.generate(c, "S")
+    ids, sc = _check(R, S, c.k, tile=2048, batch_rows=batch_rows, cta_warps=cta_warps, row_order=0)
+    ref = gpu_join(R, S, c.k, tile=2048, batch_rows=batch_rows, cta_warps=cta_warps, row_order=1)
+    np.testing.assert_array_equal(ids, ref[0])
+    np.testing.assert_array_equal(sc, ref[1])
