@@ -100,7 +100,18 @@ typedef struct {
  *  row_order:  0 (default) = rows are batched in descending order of their work estimate
  *              w_r = sum_{d in r} |I_d| (the row's share of Eq. 4's second term),
  *              so the heaviest batches are handed out first; 1 = input order.  Outputs are always in input
- *              row order and identical either way. */
+ *              row order and identical either way.
+ *  tile_begin / tile_end: restrict the query to the S tiles [tile_begin, tile_end) of the index (S ids
+ *              [tile_begin*tile, tile_end*tile)); 0 / 0 = every tile.  Out of range -> KNNJOIN_ERR_ARG.
+ *  resume_keys: NULL, or a device uint64_t[n_rows*k] of ordering keys (the out_keys of an earlier query of the
+ *              same R and k on the same index over DISJOINT tiles, input row order): the query continues
+ *              those lists, so two queries over [0, a) and [a, n_tiles) give the one-query result.
+ *  theta_in:   NULL, or a device uint64_t[n_rows] of per-row key floors (input row order): candidates of this
+ *              query's tiles with key < theta_in[r] are not kept (0 = no floor).  S-sharded multi-GPU (f2,
+ *              SURVEY.md §8(f)): the k-th key a row reached on ANY shard bounds the global k-th key from
+ *              below, so a shard may drop its candidates below the maximum over shards -- the merged result
+ *              is unchanged, and the floor tightens the pruning of head-feature completions (the threshold
+ *              carried from previous computation).  Keys equal to the floor are kept. */
 typedef struct {
   int32_t batch_rows;
   int64_t* counters;
@@ -110,6 +121,10 @@ typedef struct {
   int32_t cta_warps;
   int32_t tiles_per_pass;
   int32_t row_order;
+  int64_t tile_begin;
+  int64_t tile_end;
+  const uint64_t* resume_keys;
+  const uint64_t* theta_in;
 } knnjoin_query_options;
 
 typedef struct knnjoin_index knnjoin_index; /* opaque HOST handle; borrows the caller's index storage */

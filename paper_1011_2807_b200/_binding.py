@@ -38,7 +38,8 @@ class _Options(ctypes.Structure):
 class _QueryOptions(ctypes.Structure):
     _fields_ = [("batch_rows", ctypes.c_int32), ("counters", ctypes.c_void_p), ("ev_begin", ctypes.c_void_p),
                 ("ev_end", ctypes.c_void_p), ("phase_cycles", ctypes.c_void_p), ("cta_warps", ctypes.c_int32),
-                ("tiles_per_pass", ctypes.c_int32), ("row_order", ctypes.c_int32)]
+                ("tiles_per_pass", ctypes.c_int32), ("row_order", ctypes.c_int32), ("tile_begin", ctypes.c_int64),
+                ("tile_end", ctypes.c_int64), ("resume_keys", ctypes.c_void_p), ("theta_in", ctypes.c_void_p)]
 
 
 class _IndexInfo(ctypes.Structure):
@@ -214,15 +215,22 @@ def knnjoin_index_stats(index: Index) -> dict:
 def knnjoin_query(index: Index, R: DeviceCSR, k: int, want_keys: bool = False, want_ids: bool = True,
                   batch_rows: int = 0, counters: torch.Tensor | None = None, events=None, stream=None,
                   workspace: torch.Tensor | None = None, phase_cycles: torch.Tensor | None = None,
-                  cta_warps: int = 0, tiles_per_pass: int = 0, row_order: int = 0):
-    """Returns (ids int32 [n,k], scores float32 [n,k], keys uint64-as-int64 [n,k] or None)."""
+                  cta_warps: int = 0, tiles_per_pass: int = 0, row_order: int = 0, tile_range=(0, 0),
+                  resume_keys: torch.Tensor | None = None, theta_in: torch.Tensor | None = None):
+    """Returns (ids int32 [n,k], scores float32 [n,k], keys uint64-as-int64 [n,k] or None).
+    tile_range / resume_keys (int64 [n,k]) / theta_in (int64 [n]): see knnjoin_query_options."""
+    for t, shape in ((resume_keys, (R.n_rows, k)), (theta_in, (R.n_rows,))):
+        if t is not None and (tuple(t.shape) != shape or t.dtype != torch.int64 or not t.is_contiguous()):
+            raise ValueError(f"expected a contiguous int64 tensor of shape {shape}")
     cR = R._c()
     if events and (events[0].cuda_event == 0 or events[1].cuda_event == 0):
         raise ValueError("timing events must have been recorded once (so their cudaEvent handles exist)")
     qo = _QueryOptions(batch_rows, counters.data_ptr() if counters is not None else 0,
                        events[0].cuda_event if events else 0, events[1].cuda_event if events else 0,
                        phase_cycles.data_ptr() if phase_cycles is not None else 0, cta_warps, tiles_per_pass,
-                       row_order)
+                       row_order, tile_range[0], tile_range[1],
+                       resume_keys.data_ptr() if resume_keys is not None else 0,
+                       theta_in.data_ptr() if theta_in is not None else 0)
     wbytes = _lib.knnjoin_query_workspace_bytes(index.handle, ctypes.byref(cR), k, ctypes.byref(qo))
     if wbytes == 0:
         raise KnnJoinError(1, "knnjoin_query_workspace_bytes", knnjoin_last_error())

@@ -55,6 +55,9 @@ struct QP {
   const uint32_t* batch_nruns;
   const double* inv_sigma;
   uint32_t* batch_counter;
+  int64_t t0, t1;           // S tiles [t0, t1) of the index this query covers
+  const uint64_t* theta_in; // [n_r] per-row key floor (input row order): keys below it are not kept, or nullptr
+  const uint64_t* resume;   // [n_r][k] keys of an earlier query over other tiles to continue from, or nullptr
   int64_t tiles_per_pass;   // S tiles per pass: all batches sweep pass 0, then pass 1, ... (L2 locality)
   int64_t n_passes;
   uint64_t* state_keys;     // [n_r][k] top-k keys carried between passes (n_passes > 1)
@@ -424,8 +427,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
     if (item >= n_items) break;
     const int64_t pass = item / p.n_batches;
     const int64_t batch = item - pass * p.n_batches;
-    const int64_t t_begin = pass * p.tiles_per_pass;
-    const int64_t t_end = min(p.NT, t_begin + p.tiles_per_pass);
+    const int64_t t_begin = p.t0 + pass * p.tiles_per_pass;
+    const int64_t t_end = min(p.t1, t_begin + p.tiles_per_pass);
     const bool last_pass = pass == p.n_passes - 1;
     const int64_t row0 = batch * B;
     const int nb = (int)min((int64_t)B, p.n_r - row0);
@@ -453,6 +456,19 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
           if (pos < k) L[b][s] = __ldcg((const unsigned long long*)p.state_keys + (size_t)(row0 + b) * k + pos);
         }
         own[b] = list_kth<KS>(L[b], k);
+      } else if (pass == 0 && p.resume && warp == 0 && b < nb) {  // continue an earlier query's lists
+        const int64_t r = p.perm ? (int64_t)p.perm[row0 + b] : row0 + b;
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+          const int pos = s * 32 + lane;
+          if (pos < k) L[b][s] = __ldg((const unsigned long long*)p.resume + (size_t)r * k + pos);
+        }
+        own[b] = list_kth<KS>(L[b], k);
+      }
+      if (p.theta_in && b < nb) {  // floor from other S shards (f2): keep keys >= floor only
+        const int64_t r = p.perm ? (int64_t)p.perm[row0 + b] : row0 + b;
+        const uint64_t f = __ldg((const unsigned long long*)p.theta_in + r);
+        if (f > 0 && f - 1 > own[b]) own[b] = f - 1;
       }
     }
     if (warp == 0 && lane == 0) {
@@ -1223,6 +1239,12 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
               qopt ? qopt->cta_warps : 0, idx->tile, k);
     return KNNJOIN_ERR_UNSUPPORTED;
   }
+  if (qopt && (qopt->tile_begin < 0 || qopt->tile_end < 0 || qopt->tile_begin > idx->n_tiles ||
+               qopt->tile_end > idx->n_tiles || (qopt->tile_end > 0 && qopt->tile_begin > qopt->tile_end))) {
+    set_error("tile range [%lld, %lld) outside [0, %lld]", (long long)qopt->tile_begin, (long long)qopt->tile_end,
+              (long long)idx->n_tiles);
+    return KNNJOIN_ERR_ARG;
+  }
   const int B = sh.B;
   QueryWs W;
   query_ws_layout(R->n_rows, R->nnz, B, k, &W);
@@ -1302,6 +1324,10 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
   p.d = idx->d;
   p.T = idx->tile;
   p.NT = idx->n_tiles;
+  p.t0 = qopt ? qopt->tile_begin : 0;
+  p.t1 = (qopt && qopt->tile_end > 0) ? qopt->tile_end : idx->n_tiles;
+  p.theta_in = qopt ? qopt->theta_in : nullptr;
+  p.resume = qopt ? qopt->resume_keys : nullptr;
   p.s_id_base = idx->s_id_base;
   p.head_smem = idx->n_head_host != 0 ? 1 : 0;  // -1 (unknown) keeps the head tables
   p.n_r = R->n_rows;
@@ -1326,9 +1352,10 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
       tpp = (int64_t)((double)(l2 > 0 ? l2 : (96 << 20)) / 3.0 / (per_tile > 1.0 ? per_tile : 1.0));
       if (tpp < 1) tpp = 1;
     }
-    if (tpp > idx->n_tiles) tpp = idx->n_tiles > 0 ? idx->n_tiles : 1;
+    const int64_t span = p.t1 - p.t0;
+    if (tpp > span) tpp = span > 0 ? span : 1;
     p.tiles_per_pass = tpp;
-    p.n_passes = idx->n_tiles > 0 ? (idx->n_tiles + tpp - 1) / tpp : 1;
+    p.n_passes = span > 0 ? (span + tpp - 1) / tpp : 1;  // an empty range still runs one (tile-less) pass
   }
   p.state_keys = state_keys;
   p.pass_done = pass_done;

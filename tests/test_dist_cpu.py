@@ -43,7 +43,7 @@ def _host_merge(gathered, k):
     return out_ids, out_sc
 
 
-def _worker(rank, world, port, cfg_name, n_r, n_s, q):
+def _worker(rank, world, port, cfg_name, n_r, n_s, q, theta=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -60,21 +60,48 @@ def _worker(rank, world, port, cfg_name, n_r, n_s, q):
             ids, sc = oracle.knn(R, S_shard, c.k, s_id_base=lo)
             return torch.from_numpy(_keys(ids, sc))
 
-        ids, sc = kdist.sharded_join(local, lambda g: _host_merge(g, c.k))
+        if not theta:
+            ids, sc = kdist.sharded_join(local, lambda g: _host_merge(g, c.k))
+        else:
+            # f2 two-phase protocol: phase 1 over the first half of the shard, all_reduce(MAX) of the k-th keys,
+            # phase 2 continues with the rest keeping only keys >= floor (host model of the query's
+            # tile_range / resume_keys / theta_in semantics)
+            mid = lo + (hi - lo) // 2
+            S_a = gen.generate(c, "S", lo, mid - lo)
+            S_b = gen.generate(c, "S", mid, hi - mid)
+
+            def phase1():
+                ids, sc = oracle.knn(R, S_a, c.k, s_id_base=lo)
+                return torch.from_numpy(_keys(ids, sc))
+
+            def phase2(partial, floor):
+                ids, sc = oracle.knn(R, S_b, c.k, s_id_base=mid)
+                rest = _keys(ids, sc)
+                f = floor.numpy()[:, None]
+                rest = np.where(rest >= f, rest, 0)
+                both = np.sort(np.concatenate([partial.numpy(), rest], axis=1).view(np.uint64), axis=1)[:, ::-1]
+                seen_floor.append(int((rest == 0).sum()))
+                return torch.from_numpy(np.ascontiguousarray(both[:, :c.k]).view(np.int64))
+
+            seen_floor = []
+            ids, sc = kdist.sharded_join_theta(phase1, phase2, lambda g: _host_merge(g, c.k), c.k)
         q.put((rank, ids, sc))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("cfg_name,n_r,n_s", [("C1", 40, 3001), ("C5", 6, 2000)])
-def test_sharded_join_world2_gloo(cfg_name, n_r, n_s):
+@pytest.mark.parametrize("cfg_name,n_r,n_s,theta", [("C1", 40, 3001, False), ("C5", 6, 2000, False),
+                                                    ("C1", 40, 3001, True), ("C5", 6, 2000, True)])
+def test_sharded_join_world2_gloo(cfg_name, n_r, n_s, theta):
+    """world 2: plain S-sharded join, and the f2 two-phase protocol with cross-rank k-th-key floors; both must
+    give the oracle's single-S lists bit for bit."""
     import gen
     import oracle
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg_name, n_r, n_s, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg_name, n_r, n_s, q, theta)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]

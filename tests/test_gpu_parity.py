@@ -309,3 +309,61 @@ def test_row_order_identical(name, batch_rows, cta_warps):
     ref = gpu_join(R, S, c.k, tile=2048, batch_rows=batch_rows, cta_warps=cta_warps, row_order=1)
     np.testing.assert_array_equal(ids, ref[0])
     np.testing.assert_array_equal(sc, ref[1])
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C5"])
+def test_tile_range_resume_identical(name):
+    """tile_range + resume_keys: queries over [0, 1), [1, a), [a, NT) chained through resume_keys == one
+    query over every tile, bit for bit (keys included); an empty range passes the resumed lists through."""
+    import paper_1011_2807_b200 as kj
+    c = gen.CONFIGS[name].scaled(70, 14000)
+    R, S = gen.generate(c, "R"), gen.generate(c, "S")
+    dS, dR = kj.DeviceCSR.from_host(S), kj.DeviceCSR.from_host(R)
+    idx = kj.knnjoin_build_index(dS, c.d, tile=2048)
+    NT = kj.knnjoin_index_stats(idx)["n_tiles"]
+    assert NT >= 4
+    full = kj.knnjoin_query(idx, dR, c.k, want_keys=True)
+    a = NT // 2
+    keys = None
+    for rng in ((0, 1), (1, a), (a, a), (a, NT)):
+        ids, sc, keys = kj.knnjoin_query(idx, dR, c.k, want_keys=True, tile_range=rng, resume_keys=keys)
+    torch.cuda.synchronize()
+    for x, y in zip(full, (ids, sc, keys)):
+        np.testing.assert_array_equal(x.cpu().numpy(), y.cpu().numpy())
+    with pytest.raises(kj.KnnJoinError):
+        kj.knnjoin_query(idx, dR, c.k, tile_range=(1, NT + 1))
+
+
+@pytest.mark.parametrize("name", ["C2", "C1", "C5"])
+def test_theta_floor_two_shards_merge_exact(name):
+    """f2 on one GPU: two S shards (s_id_base), phase 1 over each shard's first tile, floor = max over shards
+    of the rows' k-th keys, phase 2 over the remaining tiles with resume_keys + theta_in; knnjoin_merge of the
+    two lists == the single-index result bit for bit, and phase 2 keeps no key of its own tiles below the
+    floor."""
+    import paper_1011_2807_b200 as kj
+    c = gen.CONFIGS[name].scaled(90, 24000)
+    R, S = gen.generate(c, "R"), gen.generate(c, "S")
+    dR = kj.DeviceCSR.from_host(R)
+    full_ids, full_sc, full_keys = gpu_join(R, S, c.k, tile=2048, want_keys=True)
+    half = S.n_rows // 2
+    shards = [(0, S.take_rows(np.arange(0, half))), (half, S.take_rows(np.arange(half, S.n_rows)))]
+    idxs = [kj.knnjoin_build_index(kj.DeviceCSR.from_host(part), c.d, s_id_base=base, tile=2048)
+            for base, part in shards]
+    p1 = [kj.knnjoin_query(ix, dR, c.k, want_keys=True, want_ids=False, tile_range=(0, 1))[2] for ix in idxs]
+    floor = torch.maximum(p1[0][:, c.k - 1], p1[1][:, c.k - 1]).contiguous()
+    p2 = []
+    for ix, part in zip(idxs, p1):
+        NT = kj.knnjoin_index_stats(ix)["n_tiles"]
+        p2.append(kj.knnjoin_query(ix, dR, c.k, want_keys=True, want_ids=False, tile_range=(1, NT),
+                                   resume_keys=part, theta_in=floor)[2])
+    for part, fin in zip(p1, p2):  # keys of phase 2 are either resumed or >= floor
+        fin_np, part_np, f = fin.cpu().numpy(), part.cpu().numpy(), floor.cpu().numpy()
+        for i in range(R.n_rows):
+            new = set(fin_np[i][fin_np[i] != 0]) - set(part_np[i])
+            assert all(x >= f[i] for x in new)
+    s_dtype = kj.BINARY if S.values is None else kj.INT8
+    ids, sc, mk = kj.knnjoin_merge(torch.stack(p2), dR, c.d, s_dtype, c.k, want_keys=True)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(ids.cpu().numpy(), full_ids)
+    np.testing.assert_array_equal(sc.cpu().numpy(), full_sc.astype(np.float32))
+    np.testing.assert_array_equal(mk.cpu().numpy(), full_keys)
