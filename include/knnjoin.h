@@ -104,8 +104,10 @@ typedef struct {
  *  tile_begin / tile_end: restrict the query to the S tiles [tile_begin, tile_end) of the index (S ids
  *              [tile_begin*tile, tile_end*tile)); 0 / 0 = every tile.  Out of range -> KNNJOIN_ERR_ARG.
  *  resume_keys: NULL, or a device uint64_t[n_rows*k] of ordering keys (the out_keys of an earlier query of the
- *              same R and k on the same index over DISJOINT tiles, input row order): the query continues
- *              those lists, so two queries over [0, a) and [a, n_tiles) give the one-query result.
+ *              same R and k over DISJOINT S ids -- other tiles of this index, or another index with a disjoint
+ *              s_id_base range; input row order): the query continues those lists, so two queries over [0, a)
+ *              and [a, n_tiles) give the one-query result, and S blocks streamed from host memory one index at
+ *              a time give the one-index result (f4, Alg. 1's block nested loop).
  *  theta_in:   NULL, or a device uint64_t[n_rows] of per-row key floors (input row order): candidates of this
  *              query's tiles with key < theta_in[r] are not kept (0 = no floor).  S-sharded multi-GPU (f2,
  *              SURVEY.md §8(f)): the k-th key a row reached on ANY shard bounds the global k-th key from

@@ -367,3 +367,20 @@ def test_theta_floor_two_shards_merge_exact(name):
     np.testing.assert_array_equal(ids.cpu().numpy(), full_ids)
     np.testing.assert_array_equal(sc.cpu().numpy(), full_sc.astype(np.float32))
     np.testing.assert_array_equal(mk.cpu().numpy(), full_keys)
+
+
+@pytest.mark.parametrize("name,blocks", [("C2", 3), ("C5", 4), ("C1", 1)])
+def test_streamed_join_equals_single_index(name, blocks):
+    """f4: S in pinned host memory streamed block by block (double-buffered copies, top-k lists resumed across
+    blocks) == one index over all of S, bit for bit; ragged last block."""
+    from paper_1011_2807_b200 import stream
+    import paper_1011_2807_b200 as kj
+    c = gen.CONFIGS[name].scaled(50, 20001)
+    R, S = gen.generate(c, "R"), gen.generate(c, "S")
+    full_ids, full_sc, full_keys = gpu_join(R, S, c.k, want_keys=True)
+    pS = stream.PinnedS.from_host(S, block_rows=(S.n_rows + blocks - 1) // blocks)
+    ids, sc, keys = stream.streamed_join(pS, kj.DeviceCSR.from_host(R), c.d, c.k, want_keys=True)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(ids.cpu().numpy(), full_ids)
+    np.testing.assert_array_equal(sc.cpu().numpy(), full_sc.astype(np.float32))
+    np.testing.assert_array_equal(keys.cpu().numpy(), full_keys)

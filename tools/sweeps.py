@@ -83,6 +83,49 @@ def main():
             r = point(cfg, study, x)
             print(json.dumps(r), flush=True)
             f.write(json.dumps(r) + "\n")
+        for r in buffer_study():
+            print(json.dumps(r), flush=True)
+            f.write(json.dumps(r) + "\n")
+
+
+def buffer_study():
+    """Fig. 4 analogue for f4: C4's laws, |R| = 10,000 against |S| = 10,000,000 held in pinned
+    host memory and streamed through HBM in blocks (paper.stream.streamed_join: copies on a copy stream,
+    double-buffered, top-k lists resumed across blocks); host->device copies inside the timed region.  The
+    first line is S resident in HBM (one index, no copies) for reference."""
+    from paper_1011_2807_b200 import stream
+    cfg = gen.CONFIGS["C4"].scaled(10_000, 10_000_000)
+    R, S = gen.generate(cfg, "R"), gen.generate(cfg, "S")
+    dR = kj.DeviceCSR.from_host(R)
+    V = visits(R, S, cfg.d)
+
+    def timed(fn):
+        for _ in range(1):
+            fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(3):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    dS = kj.DeviceCSR.from_host(S)
+    ms = timed(lambda: kj.knnjoin_query(kj.knnjoin_build_index(dS, cfg.d), dR, cfg.k))
+    del dS
+    base = {"study": "buffer", "law": "C4", "R_rows": R.n_rows, "S_rows": S.n_rows, "d": cfg.d, "k": cfg.k,
+            "visits": V}
+    yield dict(base, x="resident", blocks=1, ms=round(ms, 3), pairs_per_s=R.n_rows * S.n_rows / (ms * 1e-3))
+    for nblk in (1, 2, 4, 8, 16):
+        pS = stream.PinnedS.from_host(S, block_rows=(S.n_rows + nblk - 1) // nblk)
+        ms = timed(lambda: stream.streamed_join(pS, dR, cfg.d, cfg.k))
+        h2d = S.indptr.nbytes + S.indices.nbytes
+        yield dict(base, x=f"streamed/{nblk}", blocks=nblk, ms=round(ms, 3),
+                   pairs_per_s=R.n_rows * S.n_rows / (ms * 1e-3), h2d_bytes=h2d, h2d_gbs=h2d / (ms * 1e-3) / 1e9)
+        del pS
 
 
 if __name__ == "__main__":
