@@ -761,7 +761,45 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
               }
             }
           }
-        } else
+        }
+        // deferred exact completion of queued (row, column) pairs: lane l completes entry l -- the head part
+        // from the lookup tables, added to the partial score left in the score array, which it then zeroes
+        int qn = 0;  // queued pairs (warp-uniform)
+        auto flush = [&]() {
+          if (qn == 0) return;
+          uint64_t key = 0;
+          int pb = -1;
+          if (lane < qn) {
+            const uint32_t ent = s_queue[lane];
+            pb = (int)(ent >> 16);
+            const int cl = (int)(ent & 0xFFFFu);  // column within the tile
+            const uint32_t w = __ldg(p.head_cols + (size_t)t * T + cl);
+            uint32_t* ap = acc + (size_t)pb * TS + cl;
+            uint32_t sc = *ap;
+            *ap = 0;
+            const uint32_t* lutb = s_lut + pb * 16;
+            for (int g = 0; g < n_groups; ++g) sc += lutb[g * B * 16 + ((w >> (4 * g)) & 15u)];
+            uint64_t thb = th[0];
+#pragma unroll
+            for (int b = 1; b < B; ++b)
+              if (pb == b) thb = th[b];
+            key = make_key(sc, gbase + (uint32_t)cl);
+            if (!(sc && key > thb)) key = 0;  // the exact score does not beat this row's theta
+          }
+          __syncwarp();
+          if (__ballot_sync(0xffffffffu, key != 0)) {
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+              if (__ballot_sync(0xffffffffu, key != 0 && pb == b)) {
+                const int n = list_offer_lanes<KS>(L[b], pb == b ? key : 0, th[b], k, lane);
+                n_inserts += (lane == 0) ? n : 0;
+                if (n) publish(b);
+              }
+            }
+          }
+          qn = 0;
+        };
+        if (n_groups)
         for (int c = 0; c < cols; c += 128) {
           const int col = cbase + c + lane * 4;
           const uint32_t g0 = gbase + (uint32_t)col;
@@ -776,6 +814,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
             }
           }
           bool plain = n_groups == 0;
+          uint32_t keep = 0;  // bit 4b+j: pair left in the score array for the deferred completion
           if (n_groups) {
             const uint32_t hw[4] = {hq.x, hq.y, hq.z, hq.w};
             if (c + 128 < cols) hq = __ldg((const uint4*)(hcols + c + 128));  // next step's head words
@@ -801,7 +840,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
               }
             }
             const int npend = __reduce_add_sync(0xffffffffu, __popc(pend));
-            if (npend > 64) {
+            if (npend > 32) {
               // many pairs may reach theta (the first tiles of a batch, theta still low): complete every pair
               // from the tables and take the plain filter below
 #pragma unroll 1
@@ -816,59 +855,25 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
               }
               plain = true;
             } else if (npend) {
-              // exact completion, 32 pending pairs of the warp at a time: compact (lane, pair) into the queue,
-              // then lane l completes entry l
-              uint32_t touched = 0;
-              const uint32_t* wcols = p.head_cols + (size_t)t * T + cbase + c;
-              do {
-                const int cnt = __popc(pend);
-                int excl = cnt;
+              // exact completion is deferred: the pending pairs are appended to the warp's queue (their partial
+              // scores stay in the score array) and completed 32 at a time, one per lane
+              if (qn + npend > 32) flush();
+              int excl = __popc(pend);
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                  const int y = __shfl_up_sync(0xffffffffu, excl, o);
-                  if (lane >= o) excl += y;
-                }
-                const int total = __shfl_sync(0xffffffffu, excl, 31);
-                excl -= cnt;
-                for (int e = excl; e < 32 && pend; ++e) {
-                  const int i = __ffs(pend) - 1;
-                  pend &= pend - 1;
-                  s_queue[e] = ((uint32_t)lane << 4) | (uint32_t)i;
-                }
-                __syncwarp();
-                uint64_t key = 0;
-                int pb = -1;
-                if (lane < min(total, 32)) {
-                  const uint32_t ent = s_queue[lane];
-                  const int i = ent & 15;
-                  pb = i >> 2;
-                  const int cl = (int)(ent >> 4) * 4 + (i & 3);  // column within this 128-column step
-                  const uint32_t w = __ldg(wcols + cl);
-                  uint32_t sc = acc[(size_t)pb * TS + cbase + c + cl];
-                  const uint32_t* lutb = s_lut + pb * 16;
-                  for (int g = 0; g < n_groups; ++g) sc += lutb[g * B * 16 + ((w >> (4 * g)) & 15u)];
-                  uint64_t thb = th[0];
-#pragma unroll
-                  for (int b = 1; b < B; ++b)
-                    if (pb == b) thb = th[b];
-                  key = make_key(sc, gbase + (uint32_t)(cbase + c + cl));
-                  if (!(sc && key > thb)) key = 0;  // the exact score does not beat this row's theta
-                }
-                __syncwarp();
-                if (__ballot_sync(0xffffffffu, key != 0)) {
-#pragma unroll
-                  for (int b = 0; b < B; ++b) {
-                    if (__ballot_sync(0xffffffffu, key != 0 && pb == b)) {
-                      const int n = list_offer_lanes<KS>(L[b], pb == b ? key : 0, th[b], k, lane);
-                      n_inserts += (lane == 0) ? n : 0;
-                      touched |= (n ? 1u : 0u) << b;
-                    }
-                  }
-                }
-              } while (__any_sync(0xffffffffu, pend != 0));
-#pragma unroll
-              for (int b = 0; b < B; ++b)
-                if (touched & (1u << b)) publish(b);
+              for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, excl, o);
+                if (lane >= o) excl += y;
+              }
+              excl -= __popc(pend);
+              uint32_t pp = pend;
+              for (int e = qn + excl; pp; ++e) {
+                const int i = __ffs(pp) - 1;
+                pp &= pp - 1;
+                s_queue[e] = ((uint32_t)(i >> 2) << 16) | (uint32_t)(col + (i & 3));
+              }
+              qn += npend;
+              __syncwarp();
+              keep = pend;
             }
           }
           if (plain) {
@@ -892,8 +897,14 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
           }
 #pragma unroll
           for (int b = 0; b < B; ++b)
-            if (b < nb) *(uint4*)(acc + (size_t)b * TS + col) = make_uint4(0, 0, 0, 0);
+            if (b < nb) {  // zero-fill, except queued pairs (their completion reads and then zeroes them)
+              const uint32_t kb = keep >> (4 * b);
+              *(uint4*)(acc + (size_t)b * TS + col) =
+                  make_uint4(kb & 1u ? v[b][0] : 0u, kb & 2u ? v[b][1] : 0u, kb & 4u ? v[b][2] : 0u,
+                             kb & 8u ? v[b][3] : 0u);
+            }
         }
+        flush();
         __syncthreads();
         phase_mark(3);
       }
