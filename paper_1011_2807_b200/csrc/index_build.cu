@@ -25,9 +25,10 @@
 //   4. head selection: CUB descending sort of (df, f) over the d features, k_head_select
 //   5. k_units: units(key) = ceil(count/8) (0 for head features); CUB exclusive scan: off = scan(units)
 //   6. k_fill_pads, k_scatter (posting of sorted rank rho at position rho of its slice), k_block_layout:
-//      inside every full 256-posting block (32 units) the postings are ordered by shared-memory bank
-//      (id mod 32), so slot j of the units holds postings of ~distinct banks; the final partial block of
-//      m units gets the same bank order
+//      in slices of at least 32 units every block (256 postings, or the final partial one) is ordered by
+//      shared-memory bank (id mod 32), so slot j of the units holds postings of ~distinct banks; a slice of
+//      m < 32 units is transposed (unit i holds sorted postings i, i+m, ..., i+7m) so the lanes of a warp
+//      hit consecutive ids
 //   7. k_head_cols: one 32-bit head word per S row.
 // The paper counts this as Eq. 4's first term, sum |s_i| postings.
 #include <cub/cub.cuh>
@@ -232,7 +233,7 @@ __global__ void k_fill_pads(uint4* __restrict__ ids, int64_t units, uint32_t til
   ids[u] = make_uint4(pad, pad, pad, pad);
 }
 
-// posting of sorted rank rho goes to position rho of its slice (k_block_layout permutes inside blocks)
+// posting of sorted rank rho goes to position rho of its slice (k_block_layout permutes inside full blocks)
 __global__ void k_scatter(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, int64_t nnz,
                           const uint32_t* __restrict__ off, const uint32_t* __restrict__ first,
                           const uint32_t* __restrict__ units, uint32_t sentinel_key, uint16_t* __restrict__ ids,
@@ -241,14 +242,22 @@ __global__ void k_scatter(const uint32_t* __restrict__ keys, const uint32_t* __r
   if (i >= nnz) return;
   uint32_t key = keys[i];
   if (key >= sentinel_key || units[key] == 0) return;  // invalid feature or head feature
-  const size_t pos = (size_t)off[key] * 8 + ((uint32_t)i - first[key]);
+  // rank rho inside the slice: a slice of fewer than 32 units (one partial block of m units) is transposed here
+  // (position p -> unit p % m, slot p / m); longer slices keep rho and k_block_layout orders their blocks by
+  // bank
+  const uint32_t rho = (uint32_t)i - first[key];
+  const uint32_t U = units[key], nfull = U / 32, m = U - 32 * nfull;
+  uint32_t dst = rho;
+  if (nfull == 0) dst = (rho % m) * 8 + rho / m;  // short slice (one partial block): transpose here
+  const size_t pos = (size_t)off[key] * 8 + dst;
   const uint32_t v = vals[i];
   ids[pos] = (uint16_t)(v & 0xFFFFu);
   if (wvals) wvals[pos] = (uint8_t)(v >> 16);
 }
 
-// Warp per slice (grid-stride over keys).  Every block of m <= 32 units (256 postings when full): stable
-// counting sort by bank (id mod 32; padding last): rank r -> position r (unit r/8, slot r%8).  Deterministic: ranks come from slot-ordered
+// Warp per slice of at least 32 units (grid-stride over keys; shorter slices were transposed by k_scatter):
+// every block of m <= 32 units, stable counting sort by bank (id mod 32; padding last): rank r -> position r
+// (unit r/8, slot r%8).  Deterministic: ranks come from slot-ordered
 // match_any passes, not from the order of atomics.
 __global__ void k_block_layout(const uint32_t* __restrict__ off, const uint32_t* __restrict__ units, int64_t n_keys,
                                uint32_t tile, uint16_t* __restrict__ ids, uint8_t* __restrict__ wvals) {
@@ -261,6 +270,7 @@ __global__ void k_block_layout(const uint32_t* __restrict__ off, const uint32_t*
     const uint32_t U = units[key];
     if (U == 0) continue;
     const size_t base = (size_t)off[key] * 8;
+    if (U < 32) continue;  // short slice: transposed by k_scatter
     const uint32_t nblk = (U + 31) / 32;
     for (uint32_t blk = 0; blk < nblk; ++blk) {
       const uint32_t m = min(32u, U - 32u * blk);
@@ -281,9 +291,8 @@ __global__ void k_block_layout(const uint32_t* __restrict__ off, const uint32_t*
         }
       }
       // stable counting sort by bank (bucket 32 = padding, after every real posting; bucket 33 = lanes past
-      // the block's m units, not counted): rank r -> unit r / 8, slot r % 8.  Slot j of the m units then
-      // holds ranks j, 8 + j, ..., i.e. postings spread across the bank order: ~distinct banks per warp
-      // instruction for sparse slices, consecutive banks for dense ones.
+      // a partial block's m units, not counted): rank r -> unit r / 8, slot r % 8, so slot j of the units
+      // holds ranks j, 8 + j, ...: postings spread across the bank order
       uint32_t dst[8];
       {
         cnt[lane] = 0;
