@@ -369,7 +369,9 @@ __device__ __forceinline__ void red_add_shared(uint32_t addr, uint32_t v) {
 }
 
 
-template <int B, int KS, bool SINT8, int NW>
+// HEADS = false: instance for indexes without head features (the head tables, bounds and completions are
+// compiled out, which leaves the one-row short-slice path more registers).
+template <int B, int KS, bool SINT8, int NW, bool HEADS>
 __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_accumulate_topk(QP p) {
   constexpr int NT_ = NW * 32;        // threads per CTA
   constexpr int kCap = kcap(NW);      // runs staged per chunk
@@ -409,8 +411,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
   };
   unsigned long long n_visits = 0, n_inserts = 0, n_complete = 0, n_skipped = 0;
   const uint64_t l2pol = l2_policy_normal();
-  const int n_head = p.head_smem ? p.head_feat[kMaxHead] : 0;  // host guarantees head_smem when n_head > 0
-  const int n_groups = (n_head + 3) >> 2;
+  const int n_head = (HEADS && p.head_smem) ? p.head_feat[kMaxHead] : 0;  // host: head_smem when n_head > 0
+  const int n_groups = HEADS ? (n_head + 3) >> 2 : 0;
 
   for (int i = tid; i < (int)(acc_region_bytes(B, T, k, NW) / 16); i += NT_) ((uint4*)acc)[i] = make_uint4(0, 0, 0, 0);
 
@@ -1122,10 +1124,10 @@ __global__ void k_sorted_len(const int64_t* __restrict__ indptr, const int32_t* 
   len[i] = indptr[r + 1] - indptr[r];
 }
 
-template <int B, int KS, bool SINT8, int NW>
+template <int B, int KS, bool SINT8, int NW, bool HEADS>
 cudaError_t launch_main4(const QP& p, int sms, cudaStream_t st) {
   const size_t sm = smem_bytes(B, p.T, p.k, NW, p.head_smem != 0);
-  auto kern = k_accumulate_topk<B, KS, SINT8, NW>;
+  auto kern = k_accumulate_topk<B, KS, SINT8, NW, HEADS>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   int per_sm = 1;
@@ -1140,7 +1142,11 @@ cudaError_t launch_main4(const QP& p, int sms, cudaStream_t st) {
 template <int B, int KS, int NW>
 cudaError_t launch_main(const QP& p, int sms, cudaStream_t st) {
   if constexpr (B * KS <= 24 && B <= NW) {
-    return p.vals ? launch_main4<B, KS, true, NW>(p, sms, st) : launch_main4<B, KS, false, NW>(p, sms, st);
+    if constexpr (B == 1 && NW == 4) {  // the auto shape of indexes without head features
+      if (!p.head_smem)
+        return p.vals ? launch_main4<B, KS, true, NW, false>(p, sms, st) : launch_main4<B, KS, false, NW, false>(p, sms, st);
+    }
+    return p.vals ? launch_main4<B, KS, true, NW, true>(p, sms, st) : launch_main4<B, KS, false, NW, true>(p, sms, st);
   } else {
     return cudaErrorInvalidValue;
   }
