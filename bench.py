@@ -150,6 +150,19 @@ def visits_and_bytes(R, S, d):
     return V, b_post
 
 
+def head_visits(R, S, d, head_min_df, head_max=32):
+    """Eq. 4 visits that fall on head features (their postings are encoded as per-row words, never loaded one
+    by one): the first head_max features in (df desc, feature asc) order with df >= head_min_df (the index
+    build's rule, csrc/index_build.cu k_head_select)."""
+    if head_min_df < 0 or S.values is not None:
+        return 0
+    nR = np.bincount(R.indices[R.indices < d], minlength=d).astype(np.int64)
+    nS = np.bincount(S.indices, minlength=d).astype(np.int64)
+    order = np.lexsort((np.arange(d), -nS))[:head_max]
+    heads = order[(nS[order] >= head_min_df) & (nS[order] > 0)]
+    return int((nR[heads] * nS[heads]).sum())
+
+
 # ------------------------------------------------------------------------------------ CPU oracle leg
 def run_oracle_sample(cfg, R, S, rows, threads):
     import oracle
@@ -390,6 +403,15 @@ def bench_ours(args):
     stats = kj.knnjoin_index_stats(kj.knnjoin_build_index(dS, d, s_id_base=s_base, tile=args.tile,
                                                           head_density=args.head_density, head_max=args.head_max))
     props = torch.cuda.get_device_properties(dev)
+    # bytes the kernel actually loads one posting at a time (id-list postings) plus the head words it reads per
+    # batch and S row: the traffic that remains after the head-feature encoding (SURVEY.md §8(d) counts V*B_post)
+    Vh = head_visits(R, S, d, stats["head_min_df"], stats["head_max"] or 32)
+    n_batches_est = None
+    touched = (V - Vh) * b_post
+    if Vh:
+        bsz = args.batch_rows or 2  # the auto shape for an index with head features (pick_shape: B=2 at T=8192)
+        n_batches_est = (R.n_rows + bsz - 1) // bsz
+        touched += n_batches_est * stats["n_tiles"] * stats["tile"] * 4
     out = {
         "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -409,7 +431,12 @@ def bench_ours(args):
                      "algorithmic_bytes": V * b_post, "visits": V, "bytes_per_visit": b_post,
                      "peak_source": peak_src,
                      "note": "algorithmic posting bytes (V x B_post, SURVEY.md §8(d)); slices are re-read from L2 "
-                             "across rows, so logical GB/s can exceed HBM peak"},
+                             "across rows, so logical GB/s can exceed HBM peak",
+                     "head_visits": Vh, "touched_bytes": touched,
+                     "touched_gbs": touched / (kern_avg_max * 1e-3) / 1e9,
+                     "touched_note": "id-list postings loaded one by one ((V - head visits) x B_post) + 4-byte head "
+                                     "words read per (batch, S row); head postings are bounded/completed from the "
+                                     "words, never loaded individually"},
         "clocks": clocks,
         "gpu_launches": (launches_per_step * args.steps) if launches_per_step is not None else None,
         "breakdown": {"kernel_ms": kern_avg_max, "step_ms": ms_per_step,
