@@ -49,6 +49,32 @@ def main():
     if os.path.exists(lp):
         with open(os.path.join(ROOT, "profiles", f"{tag}_launches.txt"), "w") as f:
             f.write(launches(lp))
+    # summaries written on the box (tools/round_cycle.sh, tools/prof_configs.sh): TAG_<cfg>_full.txt + raw csv
+    for fn in sorted(os.listdir(os.path.join(ROOT, "gpurun_out"))):
+        if fn.startswith(tag + "_") and fn.endswith("_full.txt"):
+            c = fn[len(tag) + 1:-len("_full.txt")]
+            with open(os.path.join(ROOT, "gpurun_out", fn)) as fsrc, \
+                    open(os.path.join(ROOT, "profiles", f"{tag}_{c}_accumulate_full.txt"), "w") as fdst:
+                fdst.write(f"ncu --set full --clock-control none, kernel k_accumulate_topk, config {c} "
+                           f"(bench.py --config {c})\n\n")
+                fdst.write(fsrc.read())
+            rawp = os.path.join(ROOT, "gpurun_out", f"{tag}_{c}_raw.csv")
+            if os.path.exists(rawp):
+                rows = list(csv.reader(open(rawp)))
+                if len(rows) >= 3:
+                    hdr, units, vals = rows[0], rows[1], rows[2]
+                    rv = {h: (v, u) for h, u, v in zip(hdr, units, vals)}
+
+                    def num2(k):
+                        v, u = rv.get(k, ("0", "byte"))
+                        v = float(v.replace(",", "") or 0)
+                        return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+                    tp = os.path.join(ROOT, "profiles", "traffic.json")
+                    j = json.load(open(tp)) if os.path.exists(tp) else {}
+                    j[c] = num2("dram__bytes_read.sum") + num2("dram__bytes_write.sum")
+                    j["_source"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch of k_accumulate_topk, "
+                                    "ncu --set full")
+                    json.dump(j, open(tp, "w"), indent=1)
     rep = os.path.join(ROOT, "gpurun_out", f"{tag}_prof.ncu-rep")
     if os.path.exists(rep):
         import ncu_summary
