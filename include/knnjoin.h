@@ -197,7 +197,9 @@ knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr* R, int
 size_t knnjoin_merge_workspace_bytes(const knnjoin_csr* R);
 
 /* keys: uint64[P][n_rows][k] (each [n_rows][k] slab is one shard's out_keys, e.g. gathered by an NCCL
- * all-gather).  Writes the global top-k per row into out_keys / out_ids / out_scores (any may be NULL
+ * all-gather): every row of every slab sorted descending with its 0 padding last, and the P slabs from
+ * disjoint S id ranges (distinct keys), as knnjoin_query writes them.  Each merged key is placed by rank
+ * (its position plus the larger keys of the other slabs, binary searches).  Writes the global top-k per row into out_keys / out_ids / out_scores (any may be NULL
  * but not all), using R, d (the index dimensionality) and s_dtype (the dtype of S) only to recover the
  * per-row score scale, exactly as knnjoin_query computed it.
  * The merge is exact: keys encode (score, lower-id-wins) as one unsigned integer. */

@@ -34,27 +34,49 @@ __device__ unsigned long long g_bad;  // validation result word (module global, 
 
 namespace {
 
-template <int KS>
+// Warp per row.  The P lists of a row are sorted (descending, zero padding last) and hold distinct keys
+// (disjoint S id ranges), so the merged position of a key is its position in its own list plus the number of
+// larger keys in the other P-1 lists (binary searches); positions past the row's positive keys are padding.
 __global__ void k_merge(const uint64_t* __restrict__ keys, int32_t P, int64_t n, int32_t k,
                         const double* __restrict__ inv_sigma, uint64_t* out_keys, int32_t* out_ids,
                         float* out_scores) {
-  int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (r >= n) return;
-  uint64_t M[KS];
-#pragma unroll
-  for (int s = 0; s < KS; ++s) M[s] = 0;
-  uint64_t th = kKeyFloor;
-  for (int pr = 0; pr < P; ++pr) {
-    const uint64_t* src = keys + ((size_t)pr * n + r) * k;
-#pragma unroll
-    for (int s = 0; s < KS; ++s) {
-      int pos = s * 32 + lane;
-      uint64_t c = pos < k ? src[pos] : 0;
-      list_offer_lanes<KS>(M, c, th, k, lane);
+  auto list = [&](int pr) { return keys + ((size_t)pr * n + r) * k; };
+  auto count_gt = [&](const uint64_t* lst, uint64_t x) {
+    int lo = 0, hi = k;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg((const unsigned long long*)lst + mid) > x) lo = mid + 1; else hi = mid;
     }
+    return lo;
+  };
+  auto emit = [&](int pos, uint64_t key) {
+    const size_t o = (size_t)r * k + pos;
+    const uint32_t score = (uint32_t)(key >> 32);
+    if (score == 0) {
+      if (out_keys) out_keys[o] = 0;
+      if (out_ids) out_ids[o] = -1;
+      if (out_scores) out_scores[o] = 0.0f;
+    } else {
+      if (out_keys) out_keys[o] = key;
+      if (out_ids) out_ids[o] = (int32_t)(0xFFFFFFFFu - (uint32_t)key);
+      if (out_scores) out_scores[o] = (float)((double)score * inv_sigma[r]);
+    }
+  };
+  for (int i = lane; i < P * k; i += 32) {
+    const int pr = i / k, pos = i % k;
+    const uint64_t x = __ldg((const unsigned long long*)list(pr) + pos);
+    if (x == 0) continue;
+    int rank = pos;
+    for (int q = 0; q < P && rank < k; ++q)
+      if (q != pr) rank += count_gt(list(q), x);
+    if (rank < k) emit(rank, x);
   }
-  list_finalize<KS>(M, k, r, inv_sigma[r], out_keys, out_ids, out_scores, lane);
+  int npos = 0;  // positive keys over all lists (capped below by the loop)
+  for (int q = 0; q < P && npos < k; ++q) npos += count_gt(list(q), 0);
+  for (int pos = npos + lane; pos < k; pos += 32) emit(pos, 0);
 }
 
 // warp per row; records the smallest offending row in *bad (as unsigned long long)
@@ -114,11 +136,7 @@ KJ_API knnjoin_status knnjoin_merge(const uint64_t* keys, int32_t P, const knnjo
   if (e != cudaSuccess) return cuda_fail(e, "row scale");
   int64_t threads = R->n_rows * 32;
   unsigned grid = (unsigned)((threads + 255) / 256);
-  switch (ks_for_k(k)) {
-    case 1: k_merge<1><<<grid, 256, 0, st>>>(keys, P, R->n_rows, k, inv, out_keys, out_ids, out_scores); break;
-    case 4: k_merge<4><<<grid, 256, 0, st>>>(keys, P, R->n_rows, k, inv, out_keys, out_ids, out_scores); break;
-    default: k_merge<8><<<grid, 256, 0, st>>>(keys, P, R->n_rows, k, inv, out_keys, out_ids, out_scores); break;
-  }
+  k_merge<<<grid, 256, 0, st>>>(keys, P, R->n_rows, k, inv, out_keys, out_ids, out_scores);
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_merge");
   return KNNJOIN_OK;
 }

@@ -112,13 +112,15 @@ def test_configs_scaled(name, n_r, n_s, tile):
     _check(R, S, c.k, tile=tile)
 
 
-def test_sharded_merge_equals_single_index():
-    """T7: S split in P contiguous shards, P indexes with s_id_base, knnjoin_merge == one index, bit-exact."""
+@pytest.mark.parametrize("name,n_s,Ps", [("C2", 30000, (2, 3, 4)), ("C5", 16000, (2, 8)), ("C1", 9000, (3, 8))])
+def test_sharded_merge_equals_single_index(name, n_s, Ps):
+    """T7: S split in P contiguous shards, P indexes with s_id_base, knnjoin_merge == one index, bit-exact
+    (k = 100 and int8 values at C5, tie-heavy binary at C1, up to 8 shards)."""
     import paper_1011_2807_b200 as kj
-    c = gen.CONFIGS["C2"].scaled(150, 30000)
+    c = gen.CONFIGS[name].scaled(150, n_s)
     R, S = gen.generate(c, "R"), gen.generate(c, "S")
     full_ids, full_sc, full_keys = gpu_join(R, S, c.k, want_keys=True)
-    for P in (2, 3, 4):
+    for P in Ps:
         bounds = np.linspace(0, S.n_rows, P + 1).astype(np.int64)
         keys = []
         for p in range(P):
@@ -127,7 +129,8 @@ def test_sharded_merge_equals_single_index():
             keys.append(torch.from_numpy(kk))
         allk = torch.stack(keys).cuda()
         dR = kj.DeviceCSR.from_host(R)
-        ids, sc, mk = kj.knnjoin_merge(allk, dR, c.d, kj.BINARY, c.k, want_keys=True)
+        ids, sc, mk = kj.knnjoin_merge(allk, dR, c.d, kj.BINARY if S.values is None else kj.INT8, c.k,
+                                       want_keys=True)
         torch.cuda.synchronize()
         np.testing.assert_array_equal(ids.cpu().numpy(), full_ids)
         np.testing.assert_array_equal(sc.cpu().numpy(), full_sc.astype(np.float32))
