@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--row-order", type=int, default=0, help="0 work-sorted (a3), 1 input order")
     ap.add_argument("--head-density", type=float, default=0.0, help="0 auto (1/8), <0 no head features")
     ap.add_argument("--head-max", type=int, default=0, help="0 auto (64)")
+    ap.add_argument("--theta-tiles", type=int, default=0,
+                    help="N>1: f2 cross-rank threshold after this many S tiles (0 = off)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -238,10 +240,17 @@ def bench_ours(args):
     rank, world, local = dist_env()
     if world != args.gpus:
         args.gpus = world
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # KNNJOIN_BENCH_BACKEND=gloo / KNNJOIN_BENCH_DEVICE=0: functional test of the multi-rank path on a one-GPU
+    # box (tests/test_gpu_multirank.py) -- never used for a reported number
+    backend = os.environ.get("KNNJOIN_BENCH_BACKEND", "nccl")
+    dev_index = int(os.environ.get("KNNJOIN_BENCH_DEVICE", local))
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     cfg = gen.CONFIGS[args.config]
     n_s = cfg.S.n_rows
     big = cfg.scaled(None, n_s * world)
@@ -256,6 +265,13 @@ def bench_ours(args):
     dS = kj.DeviceCSR.from_host(S, dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
+    tiles_cache = {}
+
+    def idx_tiles(idx):
+        if "n" not in tiles_cache:
+            tiles_cache["n"] = kj.knnjoin_index_stats(idx)["n_tiles"]
+        return tiles_cache["n"]
+
     def step(dS_, dR_, kernel_events=None, build_event=None):
         idx = kj.knnjoin_build_index(dS_, d, s_id_base=s_base, tile=args.tile, head_density=args.head_density, head_max=args.head_max)
         if build_event is not None:
@@ -264,8 +280,18 @@ def bench_ours(args):
             ids, sc, _ = kj.knnjoin_query(idx, dR_, k, batch_rows=args.batch_rows, events=kernel_events,
                                           cta_warps=args.cta_warps, tiles_per_pass=args.tiles_per_pass, row_order=args.row_order)
             return ids, sc
-        _, _, keys = kj.knnjoin_query(idx, dR_, k, want_keys=True, want_ids=False, batch_rows=args.batch_rows,
-                                      events=kernel_events, cta_warps=args.cta_warps, tiles_per_pass=args.tiles_per_pass, row_order=args.row_order)
+        qkw = dict(want_keys=True, want_ids=False, batch_rows=args.batch_rows, cta_warps=args.cta_warps,
+                   tiles_per_pass=args.tiles_per_pass, row_order=args.row_order)
+        nt = idx_tiles(idx)
+        if args.theta_tiles > 0 and nt > 1:
+            # f2: first tiles, all_reduce(MAX) of the rows' k-th keys, remaining tiles with the floor
+            split = min(args.theta_tiles, nt - 1)
+            _, _, part = kj.knnjoin_query(idx, dR_, k, tile_range=(0, split), **qkw)
+            floor = kdist.kth_floor(part, k)
+            _, _, keys = kj.knnjoin_query(idx, dR_, k, tile_range=(split, nt), resume_keys=part, theta_in=floor,
+                                          events=kernel_events, **qkw)
+        else:
+            _, _, keys = kj.knnjoin_query(idx, dR_, k, events=kernel_events, **qkw)
         gathered = kdist.all_gather_keys(keys)  # one NCCL all_gather_into_tensor over NVLink
         ids, sc, _ = kj.knnjoin_merge(gathered, dR_, d, dS_.dtype, k)
         return ids, sc
@@ -424,6 +450,7 @@ def bench_ours(args):
                    "step": "knnjoin_build_index(S) + knnjoin_query(R,k)" + (" + all_gather + knnjoin_merge" if world > 1 else ""),
                    "l2": "flushed before every timed step (256 MiB write, outside the step's events)",
                    "parallelism": f"S-sharded x{world}" if world > 1 else "1 GPU",
+                   **({"theta_tiles": args.theta_tiles, "dist_backend": backend} if world > 1 else {}),
                    "sms": props.multi_processor_count, "l2_bytes": getattr(props, "L2_cache_size", None)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": recorded_traffic(cfg.name),

@@ -25,6 +25,8 @@ def all_gather_keys(local_keys: torch.Tensor, group=None) -> torch.Tensor:
     """[n, k] int64 keys on every rank -> [world, n, k] (rank order).  Uses all_gather_into_tensor (one NCCL
     collective); backends without it (gloo) fall back to all_gather of a list."""
     world = dist.get_world_size(group)
+    if local_keys.is_cuda and dist.get_backend(group) == "gloo":  # gloo: stage through host memory
+        return all_gather_keys(local_keys.cpu(), group).to(local_keys.device)
     out = torch.empty((world,) + tuple(local_keys.shape), dtype=local_keys.dtype, device=local_keys.device)
     try:
         dist.all_gather_into_tensor(out, local_keys.contiguous(), group=group)
@@ -47,6 +49,10 @@ def kth_floor(partial_keys: torch.Tensor, k: int, group=None) -> torch.Tensor:
     distinct keys >= its k-th key, so the global k-th key is >= the maximum over ranks: candidates below it can
     be dropped everywhere (keys are int64 views of uint64 keys < 2^63, so MAX is the key order)."""
     floor = partial_keys[:, k - 1].contiguous().clone()
+    if floor.is_cuda and dist.get_backend(group) == "gloo":  # gloo: stage through host memory
+        h = floor.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.MAX, group=group)
+        return h.to(floor.device)
     dist.all_reduce(floor, op=dist.ReduceOp.MAX, group=group)
     return floor
 
