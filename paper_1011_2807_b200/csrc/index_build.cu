@@ -22,7 +22,7 @@
 //   2. CUB stable radix sort of (key, value) pairs -- CSR order is ascending s, so each key's postings come
 //      out in ascending s (Alg. 3 inserts "in B_s scan order")
 //   3. k_seg_first / k_seg_count: run-length of equal keys -> first[key], counts[key]; k_df: df[f] = |I_f|
-//   4. head selection: CUB descending sort of (df, f) over the d features, k_head_select
+//   4. head selection (k_head_select, one CTA): features with df >= min_df ranked by (df desc, f asc)
 //   5. k_units: units(key) = ceil(count/8) (0 for head features); CUB exclusive scan: off = scan(units)
 //   6. k_fill_pads, k_scatter (posting of sorted rank rho at position rho of its slice), k_block_layout:
 //      in slices of at least 32 units every block (256 postings, or the final partial one) is ordered by
@@ -72,7 +72,7 @@ bool index_layout(const knnjoin_csr* S, int32_t d, int32_t tile, IndexLayout* L)
 namespace {
 
 struct BuildWs {
-  size_t counts_at, units_at, first_at, ka_at, kb_at, va_at, vb_at, dfk_at, dfk2_at, fv_at, fv2_at, cub_at,
+  size_t counts_at, units_at, first_at, ka_at, kb_at, va_at, vb_at, cub_at,
       cub_bytes, total;
 };
 
@@ -84,15 +84,12 @@ int end_bit_for(int64_t max_key) {
 
 bool build_ws_layout(const knnjoin_csr* S, int32_t d, const IndexLayout& L, BuildWs* W) {
   size_t nnz = (size_t)S->nnz, n_off = (size_t)L.n_off;
-  size_t sort_bytes = 0, scan_bytes = 0, dsort_bytes = 0;
+  size_t sort_bytes = 0, scan_bytes = 0;
   cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
                                                   (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)nnz, 0,
                                                   end_bit_for(L.n_off - 1));
   if (e != cudaSuccess) return false;
   e = cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n_off);
-  if (e != cudaSuccess) return false;
-  e = cub::DeviceRadixSort::SortPairsDescending(nullptr, dsort_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                                (const int32_t*)nullptr, (int32_t*)nullptr, d);
   if (e != cudaSuccess) return false;
   size_t at = 0;
   W->counts_at = at; at = align_up(at + 4 * n_off, 256);
@@ -102,14 +99,9 @@ bool build_ws_layout(const knnjoin_csr* S, int32_t d, const IndexLayout& L, Buil
   W->kb_at = at;     at = align_up(at + 4 * nnz, 256);
   W->va_at = at;     at = align_up(at + 4 * nnz, 256);
   W->vb_at = at;     at = align_up(at + 4 * nnz, 256);
-  W->dfk_at = at;    at = align_up(at + 4 * (size_t)d, 256);
-  W->dfk2_at = at;   at = align_up(at + 4 * (size_t)d, 256);
-  W->fv_at = at;     at = align_up(at + 4 * (size_t)d, 256);
-  W->fv2_at = at;    at = align_up(at + 4 * (size_t)d, 256);
   W->cub_at = at;
   W->cub_bytes = sort_bytes;
   if (scan_bytes > W->cub_bytes) W->cub_bytes = scan_bytes;
-  if (dsort_bytes > W->cub_bytes) W->cub_bytes = dsort_bytes;
   at = align_up(at + W->cub_bytes, 256);
   W->total = at;
   return true;
@@ -176,8 +168,7 @@ __global__ void k_seg_count(const uint32_t* __restrict__ keys, int64_t nnz, uint
 }
 
 // warp per feature: df[f] = sum over tiles of counts[f][t]; also the (df, f) pairs for head selection
-__global__ void k_df(const uint32_t* __restrict__ counts, int32_t d, int64_t n_tiles, int32_t* __restrict__ df,
-                     uint32_t* __restrict__ dfk, int32_t* __restrict__ fv) {
+__global__ void k_df(const uint32_t* __restrict__ counts, int32_t d, int64_t n_tiles, int32_t* __restrict__ df) {
   int64_t f = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (f >= d) return;
@@ -185,32 +176,80 @@ __global__ void k_df(const uint32_t* __restrict__ counts, int32_t d, int64_t n_t
   for (int64_t t = lane; t < n_tiles; t += 32) s += counts[f * (n_tiles + 1) + t];
 #pragma unroll
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) {
-    df[f] = (int32_t)s;
-    dfk[f] = s;
-    fv[f] = (int32_t)f;
-  }
+  if (lane == 0) df[f] = (int32_t)s;
 }
 
-// one warp: the first head_max features of the (df desc, f asc) order with df >= min_df become heads
-__global__ void k_head_select(const uint32_t* __restrict__ dfk_sorted, const int32_t* __restrict__ f_sorted,
-                              int32_t d, uint32_t min_df, int32_t head_max, int32_t* __restrict__ head_slot,
-                              int32_t* __restrict__ head_feat) {
-  const int lane = threadIdx.x;
-  int n = 0;
-  for (int base = 0; base < kMaxHead; base += 32) {
-    const int i = base + lane;
-    const bool take = i < head_max && i < d && dfk_sorted[i] >= min_df && dfk_sorted[i] > 0;
-    const uint32_t m = __ballot_sync(0xffffffffu, take);
-    if (take) {
-      head_feat[i] = f_sorted[i];
-      head_slot[f_sorted[i]] = i;
-    } else {
-      head_feat[i] = -1;
+// one CTA: the first head_max features of the (df desc, f asc) order with df >= min_df become heads.  The
+// features with df >= min_df are few (at most nnz / min_df, i.e. 8x the mean row length at the default density),
+// so they are compacted into shared memory and each is placed by its rank among them; if more than kTopCap
+// qualify, head_max rounds of "largest pair below the previous one" (block argmax) select them instead.
+constexpr int kTopThreads = 1024;
+constexpr int kTopCap = 4096;
+__global__ void __launch_bounds__(kTopThreads) k_head_select(const int32_t* __restrict__ df, int32_t d,
+                                                              uint32_t min_df, int32_t head_max,
+                                                              int32_t* __restrict__ head_slot,
+                                                              int32_t* __restrict__ head_feat) {
+  __shared__ uint32_t c_df[kTopCap];
+  __shared__ int32_t c_f[kTopCap];
+  __shared__ int s_cnt;
+  __shared__ unsigned long long s_best;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_cnt = 0;
+  for (int i = tid; i < kMaxHead; i += kTopThreads) head_feat[i] = -1;
+  __syncthreads();
+  if (head_max > 0 && min_df != 0xFFFFFFFFu) {
+    const uint32_t lo = min_df > 0 ? min_df : 1u;
+    for (int f = tid; f < d; f += kTopThreads) {
+      const uint32_t v = (uint32_t)df[f];
+      if (v >= lo) {
+        const int at = atomicAdd(&s_cnt, 1);
+        if (at < kTopCap) { c_df[at] = v; c_f[at] = f; }
+      }
     }
-    n += __popc(m);
+    __syncthreads();
+    const int cnt = s_cnt;
+    if (cnt <= kTopCap) {
+      for (int i = tid; i < cnt; i += kTopThreads) {
+        const uint32_t vi = c_df[i];
+        const int32_t fi = c_f[i];
+        int rank = 0;
+        for (int j = 0; j < cnt; ++j) rank += (c_df[j] > vi || (c_df[j] == vi && c_f[j] < fi)) ? 1 : 0;
+        if (rank < head_max) {
+          head_feat[rank] = fi;
+          head_slot[fi] = rank;
+        }
+      }
+    } else {
+      // packed order key: (df << 32) | (~f) -- larger key = earlier in (df desc, f asc)
+      unsigned long long prev = ~0ull;
+      for (int r = 0; r < head_max; ++r) {
+        unsigned long long best = 0;
+        for (int f = tid; f < d; f += kTopThreads) {
+          const uint32_t v = (uint32_t)df[f];
+          const unsigned long long key = ((unsigned long long)v << 32) | (unsigned long long)(~(uint32_t)f);
+          if (v >= lo && key < prev && key > best) best = key;
+        }
+        if (tid == 0) s_best = 0;
+        __syncthreads();
+        if (best) atomicMax(&s_best, best);
+        __syncthreads();
+        prev = s_best;
+        __syncthreads();
+        if (prev == 0) break;
+        if (tid == 0) {
+          const int32_t f = (int32_t)(~(uint32_t)prev);
+          head_feat[r] = f;
+          head_slot[f] = r;
+        }
+      }
+    }
   }
-  if (lane == 0) head_feat[kMaxHead] = n;  // n_head (heads are a prefix: df is sorted)
+  __syncthreads();
+  if (tid == 0) {
+    int n = 0;
+    if (head_max > 0 && min_df != 0xFFFFFFFFu) n = min(s_cnt, head_max);
+    head_feat[kMaxHead] = n;  // n_head (heads are a prefix of the (df desc, f asc) order)
+  }
 }
 
 __global__ void k_units(const uint32_t* __restrict__ counts, uint32_t* __restrict__ units, int64_t n,
@@ -433,10 +472,6 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   uint32_t* kb = (uint32_t*)(wb + W.kb_at);
   uint32_t* va = (uint32_t*)(wb + W.va_at);
   uint32_t* vb = (uint32_t*)(wb + W.vb_at);
-  uint32_t* dfk = (uint32_t*)(wb + W.dfk_at);
-  uint32_t* dfk2 = (uint32_t*)(wb + W.dfk2_at);
-  int32_t* fv = (int32_t*)(wb + W.fv_at);
-  int32_t* fv2 = (int32_t*)(wb + W.fv2_at);
   void* cubtmp = wb + W.cub_at;
   const uint32_t sentinel_key = (uint32_t)(L.n_off - 1);
   const uint32_t min_df = head_min_df(S, opt);
@@ -461,14 +496,9 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
     k_seg_count<<<gnnz, 256, 0, st>>>(kb, S->nnz, sentinel_key, first, counts);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_seg");
   }
-  k_df<<<(unsigned)(((int64_t)d * 32 + 255) / 256), 256, 0, st>>>(counts, d, L.n_tiles, df, dfk, fv);
+  k_df<<<(unsigned)(((int64_t)d * 32 + 255) / 256), 256, 0, st>>>(counts, d, L.n_tiles, df);
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_df");
-  {
-    size_t tb = W.cub_bytes;
-    if ((e = cub::DeviceRadixSort::SortPairsDescending(cubtmp, tb, dfk, dfk2, fv, fv2, d, 0, 32, st)) != cudaSuccess)
-      return cuda_fail(e, "df sort");
-  }
-  k_head_select<<<1, 32, 0, st>>>(dfk2, fv2, d, min_df, head_max, head_slot, head_feat);
+  k_head_select<<<1, kTopThreads, 0, st>>>(df, d, min_df, head_max, head_slot, head_feat);
   k_units<<<(unsigned)((L.n_off + 255) / 256), 256, 0, st>>>(counts, units, L.n_off, L.n_tiles, head_slot);
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_units");
   {

@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kRunThreads) k_build_runs(const int64_t* __res
                                                             const int32_t* __restrict__ perm,
                                                             const int64_t* __restrict__ rbase,
                                                             uint32_t* __restrict__ runs_f, int32_t* __restrict__ runs_q,
-                                                            uint32_t* __restrict__ batch_nruns) {
+                                                            uint32_t* __restrict__ batch_nruns, int key_bits) {
   using BRS = cub::BlockRadixSort<uint32_t, kRunThreads, kRunItems, int32_t>;
   using BScan = cub::BlockScan<int, kRunThreads>;
   __shared__ union {
@@ -229,9 +229,15 @@ __global__ void __launch_bounds__(kRunThreads) k_build_runs(const int64_t* __res
     key[it] = 0xFFFFFFFFu;
     q[it] = 0;
     if (j < ne) {
+      // row of entry j and its CSR position (unrolled selects keep rs / pre in registers)
       int b = 0;
-      while (b + 1 < nb && pre[b + 1] <= j) ++b;
-      const int64_t e = rs[b] + (j - pre[b]);
+#pragma unroll
+      for (int i = 1; i < 8; ++i) b += (j >= pre[i]) ? 1 : 0;
+      int64_t rsb = rs[0], preb = 0;
+#pragma unroll
+      for (int i = 1; i < 8; ++i)
+        if (b == i) { rsb = rs[i]; preb = pre[i]; }
+      const int64_t e = rsb + (j - preb);
       const int32_t f = indices[e];
       if (f < d) {
         key[it] = ((uint32_t)f << 3) | (uint32_t)b;
@@ -239,7 +245,7 @@ __global__ void __launch_bounds__(kRunThreads) k_build_runs(const int64_t* __res
       }
     }
   }
-  BRS(sm.sort).Sort(key, q, 0, 27);
+  BRS(sm.sort).Sort(key, q, 0, key_bits);
   __syncthreads();
 #pragma unroll
   for (int it = 0; it < kRunItems; ++it) {
@@ -278,11 +284,16 @@ __global__ void __launch_bounds__(kRunThreads) k_build_runs(const int64_t* __res
         const uint32_t kj = sm.keys[j];
         if (kj == 0xFFFFFFFFu || (kj >> 3) != f) break;
         mask |= 1u << (kj & 7u);
-        qb[kj & 7u] = s_q[j];
+        const int32_t qj = s_q[j];
+#pragma unroll
+        for (int bb = 0; bb < 8; ++bb)
+          if ((int)(kj & 7u) == bb) qb[bb] = qj;
       }
       const size_t run = base + run_idx;
       runs_f[run] = f | (mask << 24);
-      for (int b = 0; b < B; ++b) runs_q[run * B + b] = qb[b];
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+        if (b < B) runs_q[run * B + b] = qb[b];
       ++run_idx;
     }
   }
@@ -1314,21 +1325,22 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
     rbase = rb;
   }
   {
-    int64_t threads = n_batches * 32;
+    int kbits = 3;  // (feature << 3 | row) keys: bits for features < d, plus 3
+    while (kbits < 32 && ((int64_t)1 << (kbits - 3)) <= (int64_t)idx->d) ++kbits;  // invalid keys sort last
     // block-sort capacity from the mean entries per batch (x1.5 headroom); larger batches use the warp merge
     const double mean = (double)R->nnz / (double)n_batches * 1.5;
     if (mean <= kRunThreads * 4)
       k_build_runs<4><<<(unsigned)n_batches, kRunThreads, 0, st>>>(R->indptr, R->indices, R->values, R->dtype, R->n_rows,
-                                                                   idx->d, B, n_batches, sigma, perm, rbase, runs_f, runs_q, nruns);
+                                                                   idx->d, B, n_batches, sigma, perm, rbase, runs_f, runs_q, nruns, kbits);
     else if (mean <= kRunThreads * 8)
       k_build_runs<8><<<(unsigned)n_batches, kRunThreads, 0, st>>>(R->indptr, R->indices, R->values, R->dtype, R->n_rows,
-                                                                   idx->d, B, n_batches, sigma, perm, rbase, runs_f, runs_q, nruns);
+                                                                   idx->d, B, n_batches, sigma, perm, rbase, runs_f, runs_q, nruns, kbits);
     else if (mean <= kRunThreads * 16)
       k_build_runs<16><<<(unsigned)n_batches, kRunThreads, 0, st>>>(R->indptr, R->indices, R->values, R->dtype, R->n_rows,
-                                                                    idx->d, B, n_batches, sigma, perm, rbase, runs_f, runs_q, nruns);
+                                                                    idx->d, B, n_batches, sigma, perm, rbase, runs_f, runs_q, nruns, kbits);
     else
       k_build_runs<32><<<(unsigned)n_batches, kRunThreads, 0, st>>>(R->indptr, R->indices, R->values, R->dtype, R->n_rows,
-                                                                    idx->d, B, n_batches, sigma, perm, rbase, runs_f, runs_q, nruns);
+                                                                    idx->d, B, n_batches, sigma, perm, rbase, runs_f, runs_q, nruns, kbits);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_build_runs");
   }
   QP p;

@@ -149,7 +149,7 @@ def test_validate_csr():
     assert kj.knnjoin_validate_csr(oob, 8) == (3, 1)
 
 
-@pytest.mark.parametrize("name,T,hd", [("C5", 4096, 0.0), ("C2", 2048, 0.0), ("C2", 8192, 0.05)])
+@pytest.mark.parametrize("name,T,hd", [("C5", 4096, 0.0), ("C2", 2048, 0.0), ("C2", 8192, 0.05), ("C2", 2048, 1e-6)])
 def test_index_layout_matches_scipy_csc(name, T, hd):
     """T3: decode the built index (id-list slices per (feature, tile) + head-feature words) and compare with
     scipy's CSC restricted to each tile; df exact; head features are the most frequent ones."""
@@ -224,7 +224,7 @@ def test_index_layout_matches_scipy_csc(name, T, hd):
             assert b - a == (sel.sum() + 7) // 8
 
 
-@pytest.mark.parametrize("hd,hm", [(-1.0, 0), (0.0, 0), (0.01, 0), (0.01, 5), (0.3, 0)])
+@pytest.mark.parametrize("hd,hm", [(-1.0, 0), (0.0, 0), (0.01, 0), (0.01, 5), (0.3, 0), (1e-6, 0)])
 def test_head_feature_modes(hd, hm):
     """Head features (lookup-table path) and id lists give identical results for any head set."""
     c = gen.CONFIGS["C2"].scaled(300, 30000)
