@@ -36,5 +36,10 @@ for r in rows:
     agg[key] += int(r[4] or 0)
     inst[key] += int(r[7] or 0)
 tot = max(1, sum(agg.values()))
-for key, v in agg.most_common(top):
-    print(f"{100 * v / tot:5.1f}% {inst[key]:12d} {key[0]}:{key[1]:<5d} {src[key]}")
+if len(sys.argv) > 3 and sys.argv[3] == "by-inst":  # every line, by instructions executed
+    ti = max(1, sum(inst.values()))
+    for key, v in inst.most_common(top):
+        print(f"{100 * v / ti:5.1f}% inst {v:12d} stall {100 * agg[key] / tot:5.1f}% {key[0]}:{key[1]:<5d} {src[key]}")
+else:
+    for key, v in agg.most_common(top):
+        print(f"{100 * v / tot:5.1f}% {inst[key]:12d} {key[0]}:{key[1]:<5d} {src[key]}")
