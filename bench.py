@@ -152,6 +152,15 @@ def visits_and_bytes(R, S, d):
     return V, b_post
 
 
+def smem_roofline(id_visits, pairs, kernel_ms, clocks, sms):
+    mhz = (clocks or {}).get("sm_mhz") or (clocks or {}).get("sm_max_mhz") or 1965.0
+    peak = sms * 128 * mhz * 1e6 / 1e12  # TB/s
+    alg = 4 * id_visits + 8 * pairs
+    ach = alg / (kernel_ms * 1e-3) / 1e12
+    return {"bound": "smem", "achieved": ach, "peak": peak, "unit": "TB/s", "frac": ach / peak,
+            "algorithmic_bytes": alg, "peak_source": f"derived: {sms} SMs x 128 B/clk x {mhz:.0f} MHz (sampled)"}
+
+
 def head_visits(R, S, d, head_min_df, head_max=32):
     """Eq. 4 visits that fall on head features (their postings are encoded as per-row words, never loaded one
     by one): the first head_max features in (df desc, feature asc) order with df >= head_min_df (the index
@@ -475,6 +484,10 @@ def bench_ours(args):
                      "touched_note": "id-list postings loaded one by one ((V - head visits) x B_post) + 4-byte head "
                                      "words read per (batch, S row); head postings are bounded/completed from the "
                                      "words, never loaded individually"},
+        # co-bound of the one-row, short-slice configs (C1/C3/C5): shared memory.  Algorithmic shared-memory
+        # bytes of K3 = one 4-byte atomic per id-list visit + 8 bytes per pair (scan read + zero-fill) against
+        # 148 SMs x 128 B/clk at the measured SM clock (no measured smem peak exists in MEASURED_PEAKS.json)
+        "smem_roofline": smem_roofline(V - Vh, R.n_rows * n_s, kern_avg_max, clocks, props.multi_processor_count),
         "clocks": clocks,
         "gpu_launches": (launches_per_step * args.steps) if launches_per_step is not None else None,
         "breakdown": {"kernel_ms": kern_avg_max, "step_ms": ms_per_step,
