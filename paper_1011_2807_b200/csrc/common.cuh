@@ -46,6 +46,9 @@ void launch_row_scale(const knnjoin_csr* R, int32_t d, int32_t smax, double* sig
 
 // finalize / merge helpers implemented in merge.cu
 int ks_for_k(int32_t k);
+// K4: rank merge of P sorted key lists per row ([P][n][k], disjoint S ids) into the outputs
+cudaError_t launch_merge_keys(const uint64_t* keys, int32_t P, int64_t n, int32_t k, const double* inv_sigma,
+                              uint64_t* out_keys, int32_t* out_ids, float* out_scores, cudaStream_t st);
 
 }  // namespace kj
 

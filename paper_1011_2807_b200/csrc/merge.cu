@@ -79,6 +79,18 @@ __global__ void k_merge(const uint64_t* __restrict__ keys, int32_t P, int64_t n,
   for (int pos = npos + lane; pos < k; pos += 32) emit(pos, 0);
 }
 
+}  // namespace
+
+cudaError_t launch_merge_keys(const uint64_t* keys, int32_t P, int64_t n, int32_t k, const double* inv_sigma,
+                              uint64_t* out_keys, int32_t* out_ids, float* out_scores, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t threads = n * 32;
+  k_merge<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(keys, P, n, k, inv_sigma, out_keys, out_ids, out_scores);
+  return cudaGetLastError();
+}
+
+namespace {
+
 // warp per row; records the smallest offending row in *bad (as unsigned long long)
 __global__ void k_validate(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                            const void* __restrict__ values, knnjoin_dtype dt, int64_t n, int64_t nnz, int32_t d,
@@ -134,10 +146,8 @@ KJ_API knnjoin_status knnjoin_merge(const uint64_t* keys, int32_t P, const knnjo
   launch_row_scale(R, d, s_dtype == KNNJOIN_INT8 ? 127 : 1, nullptr, inv, st);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "row scale");
-  int64_t threads = R->n_rows * 32;
-  unsigned grid = (unsigned)((threads + 255) / 256);
-  k_merge<<<grid, 256, 0, st>>>(keys, P, R->n_rows, k, inv, out_keys, out_ids, out_scores);
-  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_merge");
+  if ((e = launch_merge_keys(keys, P, R->n_rows, k, inv, out_keys, out_ids, out_scores, st)) != cudaSuccess)
+    return cuda_fail(e, "k_merge");
   return KNNJOIN_OK;
 }
 

@@ -62,6 +62,8 @@ struct QP {
   int64_t n_passes;
   uint64_t* state_keys;     // [n_r][k] top-k keys carried between passes (n_passes > 1)
   uint32_t* pass_done;      // [n_batches] number of passes finished per batch
+  int32_t split;            // 1: passes are independent tile groups (small R), each writing part_keys
+  uint64_t* part_keys;      // [n_passes][n_r][k] per-group lists (split), merged by knnjoin's rank merge
   unsigned long long* counters;
   unsigned long long* phase;  // [8] cycles per phase (profiling), or nullptr
   // out
@@ -447,7 +449,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
     const int nb = (int)min((int64_t)B, p.n_r - row0);
     const int64_t run_base = p.rbase ? p.rbase[row0] : p.r_indptr[row0];
     const int nruns = (int)p.batch_nruns[batch];
-    if (pass > 0) {
+    if (pass > 0 && !p.split) {
       if (tid == 0) {
         while (*(volatile uint32_t*)&p.pass_done[batch] < (uint32_t)pass) __nanosleep(200);
         __threadfence();
@@ -462,7 +464,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
       own[b] = kKeyFloor;
 #pragma unroll
       for (int s = 0; s < KS; ++s) L[b][s] = 0;
-      if (pass > 0 && warp == 0 && b < nb) {  // warp 0 resumes from the batch's merged list
+      if (pass > 0 && !p.split && warp == 0 && b < nb) {  // warp 0 resumes from the batch's merged list
 #pragma unroll
         for (int s = 0; s < KS; ++s) {
           const int pos = s * 32 + lane;
@@ -936,6 +938,11 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
       // searches): every thread places keys independently.  Positions past the row's positive keys are
       // padding (reading c2).
       auto emit = [&](int b, int pos, uint64_t key) {
+        if (p.split) {  // independent tile groups: this group's list, merged by rank after the kernel
+          const int64_t r = p.perm ? (int64_t)p.perm[row0 + b] : row0 + b;
+          p.part_keys[((size_t)pass * p.n_r + r) * k + pos] = key;
+          return;
+        }
         if (!last_pass) {  // state is kept per sorted position
           __stcg((unsigned long long*)p.state_keys + (size_t)(row0 + b) * k + pos, (unsigned long long)key);
           return;
@@ -979,7 +986,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
         if (pos >= npos) emit(b, pos, 0);
       }
       __syncthreads();
-      if (!last_pass && tid == 0) {
+      if (!last_pass && !p.split && tid == 0) {
         __threadfence();
         atomicExch(&p.pass_done[batch], (uint32_t)(pass + 1));
       }
@@ -1011,7 +1018,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
 // ------------------------------------------------------------------------------------ host dispatch
 struct QueryWs {
   size_t sigma_at, inv_at, runs_f_at, runs_q_at, nruns_at, counter_at, state_at, done_at, wkey_at, wkey2_at,
-      perm_at, perm2_at, rlen_at, rbase_at, cub_at, cub_bytes, total;
+      perm_at, perm2_at, rlen_at, rbase_at, cub_at, cub_bytes, part_at, part_bytes, total;
 };
 
 struct Shape {
@@ -1067,7 +1074,18 @@ bool pick_shape(int T, int k, int req_B, int req_NW, int heads, Shape* out) {
   return false;
 }
 
-bool query_ws_layout(int64_t n_r, int64_t nnz_r, int B, int k, QueryWs* W) {
+// CTAs a shape keeps resident (launch bounds / shared memory of pick_shape): bounds the split-mode lists
+int ctas_per_sm(int NW) { return NW == 4 ? 6 : (NW == 8 ? 3 : 1); }
+// a query with fewer batches than kSplitWaves waves of resident CTAs splits its tiles into groups:
+// G = ceil(ctas / n_batches) below one wave, 2 between one and two waves (measured on C2-shaped serving
+// batches: more, smaller groups lose to their per-item setup and merge)
+constexpr int64_t kSplitWaves = 2;
+int64_t split_groups(int64_t n_batches, int64_t ctas) {
+  if (n_batches >= kSplitWaves * ctas) return 1;
+  return n_batches < ctas ? (ctas + n_batches - 1) / n_batches : 2;
+}
+
+bool query_ws_layout(int64_t n_r, int64_t nnz_r, int B, int NW, int k, int sms, QueryWs* W) {
   int64_t n_batches = (n_r + B - 1) / B;
   size_t at = 0;
   W->sigma_at = at;   at = align_up(at + 8 * (size_t)n_r, 256);
@@ -1094,6 +1112,12 @@ bool query_ws_layout(int64_t n_r, int64_t nnz_r, int B, int k, QueryWs* W) {
   W->rlen_at = at;    at = align_up(at + 8 * (size_t)n_r, 256);
   W->rbase_at = at;   at = align_up(at + 8 * (size_t)n_r, 256);
   W->cub_at = at;     at = align_up(at + W->cub_bytes, 256);
+  // split mode (fewer than kSplitWaves x resident CTAs batches): G tile groups x n_r rows x k keys, with
+  // G <= max(ceil(ctas / n_batches), 2) => G * n_r <= (kSplitWaves * ctas + n_batches) * B
+  const int64_t ctas = (int64_t)sms * ctas_per_sm(NW);
+  W->part_bytes = n_batches < kSplitWaves * ctas
+                      ? 8 * (size_t)k * (size_t)((kSplitWaves * ctas + n_batches) * B) : 0;
+  W->part_at = at;    at = align_up(at + W->part_bytes, 256);
   W->total = at;
   return true;
 }
@@ -1198,6 +1222,13 @@ cudaError_t launch_shape(const Shape& sh, const QP& p, int sms, cudaStream_t st)
   return cudaErrorInvalidValue;
 }
 
+int device_sms() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
 bool check_query_args(const knnjoin_index* idx, const knnjoin_csr* R, int32_t k) {
   if (!idx || !R) { set_error("index or R is NULL"); return false; }
   if (k < 1 || k > kMaxK) { set_error("k must be in [1, %d] (got %d)", kMaxK, k); return false; }
@@ -1233,7 +1264,7 @@ KJ_API size_t knnjoin_query_workspace_bytes(const knnjoin_index* idx, const knnj
       return 0;
     }
     QueryWs W;
-    query_ws_layout(R->n_rows, R->nnz, sh.B, k, &W);
+    query_ws_layout(R->n_rows, R->nnz, sh.B, sh.NW, k, device_sms(), &W);
     if (W.total > best) best = W.total;
   }
   return best;
@@ -1275,7 +1306,7 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
   }
   const int B = sh.B;
   QueryWs W;
-  query_ws_layout(R->n_rows, R->nnz, B, k, &W);
+  query_ws_layout(R->n_rows, R->nnz, B, sh.NW, k, device_sms(), &W);
   if (!workspace || workspace_bytes < W.total) { set_error("query workspace %zu < %zu bytes", workspace_bytes, W.total); return KNNJOIN_ERR_WORKSPACE; }
   if ((uintptr_t)workspace & 255) { set_error("workspace must be 256-byte aligned"); return KNNJOIN_ERR_ARG; }
   if (R->n_rows == 0) return KNNJOIN_OK;
@@ -1383,6 +1414,21 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
     }
     const int64_t span = p.t1 - p.t0;
     if (tpp > span) tpp = span > 0 ? span : 1;
+    // few batches (small R, serving): the tiles are split into G independent groups (split_groups) so that
+    // the G x n_batches items fill the resident CTAs; each group's lists go to part_keys and are merged by
+    // rank
+    p.split = 0;
+    p.part_keys = nullptr;
+    const int64_t ctas = (int64_t)device_sms() * ctas_per_sm(sh.NW);
+    if (!(qopt && qopt->tiles_per_pass) && W.part_bytes && span > 1 && n_batches < kSplitWaves * ctas) {
+      int64_t G = split_groups(n_batches, ctas);
+      if (G > span) G = span;
+      if (G > 1 && (size_t)G * (size_t)R->n_rows * (size_t)k * 8 <= W.part_bytes) {
+        tpp = (span + G - 1) / G;
+        p.split = 1;
+        p.part_keys = (uint64_t*)(wb + W.part_at);
+      }
+    }
     p.tiles_per_pass = tpp;
     p.n_passes = span > 0 ? (span + tpp - 1) / tpp : 1;  // an empty range still runs one (tile-less) pass
   }
@@ -1400,5 +1446,9 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
   e = launch_shape(sh, p, sms, st);
   if (qopt && qopt->ev_end) cudaEventRecord((cudaEvent_t)qopt->ev_end, st);
   if (e != cudaSuccess) return cuda_fail(e, "k_accumulate_topk");
+  if (p.split) {  // the tile groups' lists hold disjoint S ids: K4's rank merge gives the one-pass result
+    e = launch_merge_keys(p.part_keys, (int32_t)p.n_passes, R->n_rows, k, inv_sigma, out_keys, out_ids, out_scores, st);
+    if (e != cudaSuccess) return cuda_fail(e, "split merge");
+  }
   return KNNJOIN_OK;
 }

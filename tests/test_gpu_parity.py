@@ -387,3 +387,60 @@ def test_streamed_join_equals_single_index(name, blocks):
     np.testing.assert_array_equal(ids.cpu().numpy(), full_ids)
     np.testing.assert_array_equal(sc.cpu().numpy(), full_sc.astype(np.float32))
     np.testing.assert_array_equal(keys.cpu().numpy(), full_keys)
+
+
+def test_query_cuda_graph_replay():
+    """After the first query on an index (which reads the index statistics once), knnjoin_query is
+    stream-capturable: a CUDA graph of one query replays to the same lists, and a replay after new R weights
+    are written into the captured input buffers gives that R's lists (serving many R batches of one shape
+    against one S)."""
+    import paper_1011_2807_b200 as kj
+    c = gen.CONFIGS["C2"].scaled(64, 30000)
+    S = gen.generate(c, "S")
+    R1 = gen.generate(c, "R")
+    idx = kj.knnjoin_build_index(kj.DeviceCSR.from_host(S), c.d)
+    dR = kj.DeviceCSR.from_host(R1)
+    ref1 = kj.knnjoin_query(idx, dR, c.k)  # first query: reads the index statistics (synchronises once)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        kj.knnjoin_query(idx, dR, c.k)  # warm-up on the capture stream
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ids, sc, _ = kj.knnjoin_query(idx, dR, c.k)
+    g.replay()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(ids.cpu().numpy(), ref1[0].cpu().numpy())
+    np.testing.assert_array_equal(sc.cpu().numpy(), ref1[1].cpu().numpy())
+    # a new R of the same shape: same features, new positive weights
+    rng = np.random.default_rng(5)
+    vals = (R1.values * rng.uniform(0.1, 3.0, R1.nnz)).astype(np.float32)
+    R3 = gen.HostCSR(R1.indptr, R1.indices, vals, c.d)
+    dR.values.copy_(torch.from_numpy(vals))
+    g.replay()
+    torch.cuda.synchronize()
+    o_ids, o_sc = oracle.knn(R3, S, c.k, threads=8)
+    assert_parity(R3, S, ids.cpu().numpy().astype(np.int64), sc.cpu().numpy().astype(np.float64), o_ids, o_sc)
+    assert not np.array_equal(o_ids, ref1[0].cpu().numpy())  # the replay really computed a different join
+
+
+@pytest.mark.parametrize("name,n_r", [("C2", 16), ("C2", 300), ("C3", 40), ("C5", 24), ("C1", 100)])
+def test_split_tile_groups_identical(name, n_r):
+    """Small R (fewer batches than resident CTAs): the tiles are split into independent groups whose lists
+    are merged by rank after the kernel -- bit-identical (keys included) to the unsplit schedule
+    (tiles_per_pass given explicitly disables the split), and to the oracle."""
+    import paper_1011_2807_b200 as kj
+    c = gen.CONFIGS[name].scaled(n_r, 25000)
+    R, S = gen.generate(c, "R"), gen.generate(c, "S")
+    ids, sc = _check(R, S, c.k, tile=2048)
+    dS, dR = kj.DeviceCSR.from_host(S), kj.DeviceCSR.from_host(R)
+    idx = kj.knnjoin_build_index(dS, c.d, tile=2048)
+    split = kj.knnjoin_query(idx, dR, c.k, want_keys=True)
+    whole = kj.knnjoin_query(idx, dR, c.k, want_keys=True, tiles_per_pass=1000)
+    torch.cuda.synchronize()
+    for x, y in zip(split, whole):
+        np.testing.assert_array_equal(x.cpu().numpy(), y.cpu().numpy())
+    np.testing.assert_array_equal(ids, whole[0].cpu().numpy())
