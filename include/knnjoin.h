@@ -86,7 +86,11 @@ typedef struct {
  *              device-to-host copy that synchronises `stream` once per index).
  *  tiles_per_pass: S tiles swept by all batches before any batch moves on (0 = auto: about a third of the
  *              L2 cache worth of index per pass; the whole index when it fits).  Top-k state is carried
- *              between passes in the workspace; results do not depend on it.
+ *              between passes in the workspace; results do not depend on it.  Auto also splits the tiles
+ *              into independent groups when R has fewer batches than two waves of resident CTAs (small R,
+ *              serving): each group's lists are merged by rank after the kernel (K4), same result.
+ *  Graph capture: after the first query on an index (which reads the index statistics, see cta_warps),
+ *              knnjoin_query issues only stream-ordered work and may be captured into a CUDA graph.
  *  counters:   NULL, or a device int64_t[4] that the query ADDS into: [0] postings visited (Eq. 4 second
  *              term; head postings are counted whether or not their completion is skipped),
  *              [1] candidate inserts into the top-k lists, [2] head postings whose exact addition was skipped
