@@ -99,8 +99,8 @@ typedef struct {
  *  ev_begin / ev_end: NULL, or cudaEvent_t (as void*) recorded on `stream` immediately before and after
  *              the score-accumulation + top-k kernel, so callers can time that kernel alone.
  *  phase_cycles: NULL, or a device int64_t[8] that the query ADDS SM clock cycles into, summed over CTAs
- *              (thread 0 of each CTA): [0] staging, [1] sparse atomics, [2] head tables, [3] scan + top-k,
- *              [4] list merge + output, [5] batch fetch / setup.  Profiling aid; off when NULL.
+ *              (thread 0 of each CTA): [0] staging, [1] sparse atomics, [2] (unused), [3] scan + top-k,
+ *              [4] list merge + output, [5] batch fetch / setup + head tables.  Profiling aid; off when NULL.
  *  row_order:  0 (default) = rows are batched in descending order of their work estimate
  *              w_r = sum_{d in r} |I_d| (the row's share of Eq. 4's second term),
  *              so the heaviest batches are handed out first; 1 = input order.  Outputs are always in input

@@ -13,12 +13,10 @@
 
 namespace kj {
 
-constexpr int kWarps = 16;             // warps per CTA of the accumulation kernel
-constexpr int kThreads = kWarps * 32;  // 512
 constexpr int kMaxK = 256;
 constexpr int kDefaultTile = 8192;
 constexpr int kMaxTile = 32768;        // local ids < tile; padding ids are tile + (0..31) (dummy columns)
-constexpr int kTileQuantum = 2048;     // tile must split into kWarps column strips of 128-column chunks
+constexpr int kTileQuantum = 2048;     // tile must split into 16 warps' column strips of 128-column steps
 constexpr int kMaxHead = 32;                  // head features per index (one 32-bit word per S row)
 constexpr float kDefaultHeadDensity = 0.125f;  // df >= |S|/8 makes a feature a head candidate
 constexpr int kPadCols = 32;           // dummy score columns per row that absorb padding postings
