@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--head-max", type=int, default=0, help="0 auto (64)")
     ap.add_argument("--theta-tiles", type=int, default=0,
                     help="N>1: f2 cross-rank threshold after this many S tiles (0 = off)")
+    ap.add_argument("--prune-alpha", type=float, default=0.0,
+                    help="> 0: threshold-pruned queries (a6) with this alpha on an index built with prune=1")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -269,6 +271,9 @@ def bench_ours(args):
     d, k = cfg.d, cfg.k
     V, b_post = visits_and_bytes(R, S, d)
 
+    # index build options (a6 pruned mode: forward rows kept, head features off)
+    bkw = dict(s_id_base=s_base, tile=args.tile, head_density=args.head_density, head_max=args.head_max,
+               prune=1 if args.prune_alpha > 0 else 0, alpha=args.prune_alpha if args.prune_alpha > 0 else 0.0)
     stream = torch.cuda.current_stream()
     dR = kj.DeviceCSR.from_host(R, dev)
     dS = kj.DeviceCSR.from_host(S, dev)
@@ -282,7 +287,7 @@ def bench_ours(args):
         return tiles_cache["n"]
 
     def step(dS_, dR_, kernel_events=None, build_event=None, before_query=None):
-        idx = kj.knnjoin_build_index(dS_, d, s_id_base=s_base, tile=args.tile, head_density=args.head_density, head_max=args.head_max)
+        idx = kj.knnjoin_build_index(dS_, d, **bkw)
         if build_event is not None:
             build_event.record(stream)
         if before_query is not None:
@@ -326,16 +331,17 @@ def bench_ours(args):
 
     # per-phase SM cycles of the accumulate kernel (one untimed instrumented step)
     phase = torch.zeros(8, dtype=torch.int64, device=dev)
-    idx_p = kj.knnjoin_build_index(dS, d, s_id_base=s_base, tile=args.tile, head_density=args.head_density, head_max=args.head_max)
+    idx_p = kj.knnjoin_build_index(dS, d, **bkw)
     kj.knnjoin_query(idx_p, dR, k, batch_rows=args.batch_rows, phase_cycles=phase, cta_warps=args.cta_warps, tiles_per_pass=args.tiles_per_pass, row_order=args.row_order)
     torch.cuda.synchronize()
     ph = phase.cpu().tolist()
     cnt = torch.zeros(4, dtype=torch.int64, device=dev)
-    idx_c = kj.knnjoin_build_index(dS, d, s_id_base=s_base, tile=args.tile, head_density=args.head_density,
-                                   head_max=args.head_max)
+    idx_c = kj.knnjoin_build_index(dS, d, **bkw)
     kj.knnjoin_query(idx_c, dR, k, batch_rows=args.batch_rows, counters=cnt, cta_warps=args.cta_warps, tiles_per_pass=args.tiles_per_pass, row_order=args.row_order)
     torch.cuda.synchronize()
-    counters = dict(zip(["postings_visited", "inserts", "head_postings_skipped", "head_completions"],
+    counters = dict(zip(["postings_visited", "inserts", "head_postings_skipped", "head_completions"]
+                        if args.prune_alpha <= 0 else
+                        ["postings_visited", "inserts", "pruned_units_skipped", "pruned_completions"],
                         cnt.cpu().tolist()))
     del idx_c
     tot_ph = max(1, sum(ph[:6]))
@@ -446,8 +452,7 @@ def bench_ours(args):
 
     peak, peak_src = measured_peak()
     achieved = V * b_post / (kern_avg_max * 1e-3) / 1e9
-    stats = kj.knnjoin_index_stats(kj.knnjoin_build_index(dS, d, s_id_base=s_base, tile=args.tile,
-                                                          head_density=args.head_density, head_max=args.head_max))
+    stats = kj.knnjoin_index_stats(kj.knnjoin_build_index(dS, d, **bkw))
     props = torch.cuda.get_device_properties(dev)
     # bytes the kernel actually loads one posting at a time (id-list postings) plus the head words it reads per
     # batch and S row: the traffic that remains after the head-feature encoding (SURVEY.md §8(d) counts V*B_post)
@@ -458,6 +463,8 @@ def bench_ours(args):
         bsz = args.batch_rows or 2  # the auto shape for an index with head features (pick_shape: B=2 at T=8192)
         n_batches_est = (R.n_rows + bsz - 1) // bsz
         touched += n_batches_est * stats["n_tiles"] * stats["tile"] * 4
+    if args.prune_alpha > 0:  # a6: posting units whose loads were skipped (8 postings each, padding included)
+        touched = max(0, touched - counters["pruned_units_skipped"] * 8 * b_post)
     out = {
         "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -467,6 +474,7 @@ def bench_ours(args):
                    "nnz_R": int(R.nnz), "nnz_S_per_gpu": int(S.nnz), "tile": stats["tile"],
                    "n_tiles": stats["n_tiles"], "batch_rows": args.batch_rows or "auto",
                    "head_min_df": stats["head_min_df"], "head_max": stats["head_max"],
+                   **({"prune_alpha": args.prune_alpha} if args.prune_alpha > 0 else {}),
                    "step": "knnjoin_build_index(S) + knnjoin_query(R,k)" + (" + all_gather + knnjoin_merge" if world > 1 else ""),
                    "l2": "flushed before every timed step (256 MiB write, outside the step's events)",
                    "parallelism": f"S-sharded x{world}" if world > 1 else "1 GPU",

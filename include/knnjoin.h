@@ -61,7 +61,17 @@ typedef struct {
 
 /* Build options.  tile: S ids per tile (the S-block of Alg. 1 mapped to a shared-memory score array);
  * 0 = default 8192; must be a multiple of 2048 and <= 32768.
- * prune / alpha: reserved for the threshold-pruned mode; must be 0 / 0.
+ * prune / alpha: prune = 1 builds the index for the threshold-pruned query mode (the
+ *   r-side form of IIIB's threshold refinement, PAPER.md:161-173 and Alg. 4): the storage
+ *   additionally keeps S's forward rows (indptr, features, int8 weights) and, for INT8 S, the largest weight
+ *   of every feature, and head features are off.  alpha in (0, 1] is the default pruning aggressiveness of
+ *   queries on this index (0 = 0.25).  A pruned query, per row r and S tile, orders r's features by
+ *   c_d = q_r[d] * maxweight(d) (descending, ties by feature), takes as non-essential the longest suffix N
+ *   with sum_{d in N} c_d <= min(alpha * theta, theta - 1) (theta = the score of r's running k-th key),
+ *   skips the tile's posting slices of N, and completes exactly -- from the forward row of s against N --
+ *   every s whose partial score plus sum_{d in N, slice non-empty} c_d reaches theta.  An s that the
+ *   skipped slices alone could reach has score < theta and cannot enter.  Results are identical to the
+ *   unpruned query; only the work changes.  prune = 0: alpha must be 0.
  * head_density / head_max: "head features" (BINARY S only).  Up to head_max (0 = 32, at most 32) of the
  *   most frequent features with df >= head_density * |S| (0 = default 1/8, negative = no head features) are
  *   not stored as id lists: each S row gets one 32-bit word of head-feature bits.  During the top-k scan the
@@ -117,7 +127,12 @@ typedef struct {
  *              SURVEY.md §8(f)): the k-th key a row reached on ANY shard bounds the global k-th key from
  *              below, so a shard may drop its candidates below the maximum over shards -- the merged result
  *              is unchanged, and the floor tightens the pruning of head-feature completions (the threshold
- *              carried from previous computation).  Keys equal to the floor are kept. */
+ *              carried from previous computation).  Keys equal to the floor are kept.
+ *  prune_alpha: threshold pruning on an index built with prune = 1 (see knnjoin_options): 0 = the index's
+ *              alpha, in (0, 1] = this alpha, < 0 = off.  On an index built without prune it must be 0 or
+ *              negative.  Pruned queries run the one-row 4-warp shape (batch_rows / cta_warps must be 0 or
+ *              1 / 4).  counters [2] then counts the 16-byte posting units (8 postings, padding included) whose
+ *              loads were skipped, and [3] the exact completions ((row, S row) pairs). */
 typedef struct {
   int32_t batch_rows;
   int64_t* counters;
@@ -131,6 +146,7 @@ typedef struct {
   int64_t tile_end;
   const uint64_t* resume_keys;
   const uint64_t* theta_in;
+  float prune_alpha;
 } knnjoin_query_options;
 
 typedef struct knnjoin_index knnjoin_index; /* opaque HOST handle; borrows the caller's index storage */
@@ -147,6 +163,8 @@ typedef struct {
   knnjoin_dtype s_dtype;
   int64_t head_min_df;  /* df from which a feature may be a head feature (-1: head features off) */
   int32_t head_max;     /* cap on the number of head features (their count is known on the device only) */
+  int32_t prune;        /* 1: built for pruned queries (forward rows kept) */
+  float alpha;          /* default pruning alpha of queries on this index (prune = 1) */
 } knnjoin_index_info;
 
 /* ---- index build: Create_Inverted_List_IIB (Alg. 3 lines 5-8) on the device ------ */

@@ -39,14 +39,16 @@ class _QueryOptions(ctypes.Structure):
     _fields_ = [("batch_rows", ctypes.c_int32), ("counters", ctypes.c_void_p), ("ev_begin", ctypes.c_void_p),
                 ("ev_end", ctypes.c_void_p), ("phase_cycles", ctypes.c_void_p), ("cta_warps", ctypes.c_int32),
                 ("tiles_per_pass", ctypes.c_int32), ("row_order", ctypes.c_int32), ("tile_begin", ctypes.c_int64),
-                ("tile_end", ctypes.c_int64), ("resume_keys", ctypes.c_void_p), ("theta_in", ctypes.c_void_p)]
+                ("tile_end", ctypes.c_int64), ("resume_keys", ctypes.c_void_p), ("theta_in", ctypes.c_void_p),
+                ("prune_alpha", ctypes.c_float)]
 
 
 class _IndexInfo(ctypes.Structure):
     _fields_ = [("n_s", ctypes.c_int64), ("s_id_base", ctypes.c_int64), ("d", ctypes.c_int32),
                 ("tile", ctypes.c_int32), ("n_tiles", ctypes.c_int64), ("offsets", ctypes.c_int64),
                 ("unit_capacity", ctypes.c_int64), ("storage_bytes", ctypes.c_int64), ("s_dtype", ctypes.c_int),
-                ("head_min_df", ctypes.c_int64), ("head_max", ctypes.c_int32)]
+                ("head_min_df", ctypes.c_int64), ("head_max", ctypes.c_int32), ("prune", ctypes.c_int32),
+                ("alpha", ctypes.c_float)]
 
 
 def library_path() -> str:
@@ -185,9 +187,10 @@ def _empty_u8(nbytes: int, device) -> torch.Tensor:
 
 def knnjoin_build_index(S: DeviceCSR, d: int, s_id_base: int = 0, tile: int = 0, stream=None,
                         workspace: torch.Tensor | None = None, head_density: float = 0.0,
-                        head_max: int = 0) -> Index:
+                        head_max: int = 0, prune: int = 0, alpha: float = 0.0) -> Index:
+    """prune=1 keeps S's forward rows for threshold-pruned queries (a6; knnjoin_options.prune / alpha)."""
     cS = S._c()
-    opt = _Options(tile, 0, 0.0, head_density, head_max)
+    opt = _Options(tile, prune, alpha, head_density, head_max)
     nbytes = _lib.knnjoin_index_bytes(ctypes.byref(cS), d, ctypes.byref(opt))
     if nbytes == 0:
         raise KnnJoinError(1, "knnjoin_index_bytes", knnjoin_last_error())
@@ -216,9 +219,10 @@ def knnjoin_query(index: Index, R: DeviceCSR, k: int, want_keys: bool = False, w
                   batch_rows: int = 0, counters: torch.Tensor | None = None, events=None, stream=None,
                   workspace: torch.Tensor | None = None, phase_cycles: torch.Tensor | None = None,
                   cta_warps: int = 0, tiles_per_pass: int = 0, row_order: int = 0, tile_range=(0, 0),
-                  resume_keys: torch.Tensor | None = None, theta_in: torch.Tensor | None = None):
+                  resume_keys: torch.Tensor | None = None, theta_in: torch.Tensor | None = None,
+                  prune_alpha: float = 0.0):
     """Returns (ids int32 [n,k], scores float32 [n,k], keys uint64-as-int64 [n,k] or None).
-    tile_range / resume_keys (int64 [n,k]) / theta_in (int64 [n]): see knnjoin_query_options."""
+    tile_range / resume_keys (int64 [n,k]) / theta_in (int64 [n]) / prune_alpha: see knnjoin_query_options."""
     for t, shape in ((resume_keys, (R.n_rows, k)), (theta_in, (R.n_rows,))):
         if t is not None and (tuple(t.shape) != shape or t.dtype != torch.int64 or not t.is_contiguous()):
             raise ValueError(f"expected a contiguous int64 tensor of shape {shape}")
@@ -230,7 +234,7 @@ def knnjoin_query(index: Index, R: DeviceCSR, k: int, want_keys: bool = False, w
                        phase_cycles.data_ptr() if phase_cycles is not None else 0, cta_warps, tiles_per_pass,
                        row_order, tile_range[0], tile_range[1],
                        resume_keys.data_ptr() if resume_keys is not None else 0,
-                       theta_in.data_ptr() if theta_in is not None else 0)
+                       theta_in.data_ptr() if theta_in is not None else 0, prune_alpha)
     wbytes = _lib.knnjoin_query_workspace_bytes(index.handle, ctypes.byref(cR), k, ctypes.byref(qo))
     if wbytes == 0:
         raise KnnJoinError(1, "knnjoin_query_workspace_bytes", knnjoin_last_error())

@@ -42,6 +42,14 @@ struct QP {
   uint64_t* part_keys;      // [n_passes][n_r][k] per-group lists (split), merged by knnjoin's rank merge
   unsigned long long* counters;
   unsigned long long* phase;  // [8] cycles per phase (profiling), or nullptr
+  // threshold pruning (a6; PRUNE instances only)
+  float alpha;               // non-essential budget = min(alpha * theta, theta - 1)
+  const uint32_t* prune_suf; // [runs] per run: sum of c over the runs at or after it in c-descending order
+  const int64_t* fwd_ptr;    // [n_s + 1] forward rows of S (local row ids)
+  const int32_t* fwd_idx;    // [nnz(S)]
+  const uint8_t* fwd_val;    // [nnz(S)] INT8 S weights, or nullptr (BINARY)
+  const uint32_t* fmax;      // [d] largest S weight per feature, or nullptr (BINARY: 1)
+  int32_t prune_words;       // (d + 31) / 32: shared bitmap of the row's non-essential features
   // out
   uint64_t* out_keys;
   int32_t* out_ids;
@@ -155,8 +163,16 @@ __device__ __forceinline__ void red_add_shared(uint32_t addr, uint32_t v) {
 
 // HEADS = false: instance for indexes without head features (the head tables, bounds and completions are
 // compiled out, which leaves the one-row short-slice path more registers).
-template <int B, int KS, bool SINT8, int NW, bool HEADS>
+// PRUNE = true (B = 1, HEADS = false only): threshold pruning, SURVEY.md §8(a) a6 -- the r-side form of IIIB's
+// threshold refinement (Alg. 4).  Per tile, with theta = the score of the
+// row's running k-th key, the runs whose c-descending suffix sum (prune_suf) is <= budget =
+// min(alpha * theta, theta - 1) are non-essential (N): their slices are not loaded.  In the scan an s with
+// partial score x > 0 is completed exactly (its forward row merged against N) when x + U_N >= theta, where
+// U_N = sum of c over N's non-empty slices of the tile; any other s has score <= x + U_N < theta (or, with
+// x = 0, <= U_N <= budget < theta) and cannot enter.
+template <int B, int KS, bool SINT8, int NW, bool HEADS, bool PRUNE = false>
 __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_accumulate_topk(QP p) {
+  static_assert(!PRUNE || (B == 1 && !HEADS), "pruned instances are one-row and head-free");
   constexpr int NT_ = NW * 32;        // threads per CTA
   constexpr int kCap = kcap(NW);      // runs staged per chunk
   constexpr int IPT = (kCap + NT_ - 1) / NT_;  // staged runs per thread (the last may be partial)
@@ -181,6 +197,9 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t* s_queue = (uint32_t*)(s_misc + 8) + warp * 32;  // this warp's head-completion queue (heads only)
+  // a6: bit f set <=> feature f of the batch row is non-essential in the current tile (placed after everything
+  // else; the budget only grows within an item, so the bits of earlier tiles stay valid)
+  uint32_t* s_nbits = (uint32_t*)(smem + align_up(smem_bytes(B, T, p.k, NW, p.head_smem), 16));
   const int k = p.k;
   constexpr bool wint8 = SINT8;
   const bool timing = p.phase != nullptr && tid == 0;
@@ -261,6 +280,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
 #pragma unroll
       for (int b = 0; b < B; ++b) s_theta[b] = own[b];
     }
+    if constexpr (PRUNE)
+      for (int i = tid; i < p.prune_words; i += NT_) s_nbits[i] = 0;
     // ------------------------------------------------------------------ head tables of this batch
     if (n_groups) {
       for (int i = tid; i < kMaxHead * B; i += NT_) s_qh[i] = 0;
@@ -314,6 +335,16 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
 
     const int64_t t_stop = nruns > 0 ? t_end : t_begin;
     for (int64_t t = t_begin; t < t_stop; ++t) {
+      // a6: the non-essential budget of this tile, from the row's k-th key so far (every thread reads the same
+      // value: s_theta is only written during scans, which are fenced by __syncthreads)
+      uint32_t budget = 0;
+      if constexpr (PRUNE) {
+        const uint32_t th_s = (uint32_t)(*(volatile uint64_t*)&s_theta[0] >> 32);
+        if (th_s > 0) {
+          const double a = (double)p.alpha * (double)th_s;
+          budget = a >= (double)(th_s - 1) ? th_s - 1 : (uint32_t)a;
+        }
+      }
       for (int c0 = 0; c0 < nruns; c0 += kCap) {
         // ---------------------------------------------------------------- stage chunk of runs
         // non-empty slices are compacted with their position P in the flattened unit stream (head
@@ -321,6 +352,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
         {
           uint32_t fm[IPT], u0[IPT], U[IPT];
           uint64_t pk[IPT], mine = 0;
+          uint32_t un_mine = 0;  // a6: c of this thread's skipped non-empty slices
 #pragma unroll
           for (int it = 0; it < IPT; ++it) {
             const int li = tid + it * NT_;  // run li of this chunk
@@ -331,12 +363,25 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
               const uint32_t* o = p.off + (size_t)(fm[it] & 0xFFFFFFu) * (size_t)(p.NT + 1) + (size_t)t;
               u0[it] = o[0];
               U[it] = o[1] - u0[it];
+              if constexpr (PRUNE) {
+                if (__ldg(p.prune_suf + run_base + i) <= budget) {  // non-essential: slice not loaded
+                  const uint32_t f = fm[it] & 0xFFFFFFu;
+                  atomicOr(&s_nbits[f >> 5], 1u << (f & 31u));
+                  if (U[it] > 0) {
+                    un_mine += (uint32_t)__ldg(p.runs_q + run_base + i) * (p.fmax ? __ldg(p.fmax + f) : 1u);
+                    n_skipped += U[it];
+                  }
+                  U[it] = 0;
+                }
+              }
             }
             pk[it] = ((uint64_t)(U[it] > 0) << 32) | U[it];
             mine += pk[it];
           }
+          if (PRUNE && c0 == 0 && tid == 0) s_misc[4] = 0;  // U_N of this tile (read after the accumulate)
           uint64_t total;
           uint64_t ex = block_exclusive_scan_u64<NW>(mine, s_warp, &total);
+          if (PRUNE && un_mine) atomicAdd((unsigned*)&s_misc[4], un_mine);
 #pragma unroll
           for (int it = 0; it < IPT; ++it) {
             if (U[it] > 0) {
@@ -522,6 +567,39 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
 #pragma unroll
           for (int b = 0; b < B; ++b) t32[b] = t32_of(th[b]);
           const uint32_t a0 = acc_s + (uint32_t)(cbase + lane * 4) * 4u;
+          // a6: U_N of this tile (0 when nothing was skipped: the plain filter)
+          const uint32_t un = PRUNE ? (uint32_t)s_misc[4] : 0u;
+          // a6 exact completion of s = local column col: add r's non-essential features that s has, merging s's
+          // forward row against the row's runs (both ascending by feature)
+          auto complete = [&](uint32_t col) -> uint32_t {
+            uint32_t add = 0;
+            if constexpr (PRUNE) {
+              const int64_t srow = t * (int64_t)T + col;
+              const int64_t e0 = __ldg(p.fwd_ptr + srow), e1 = __ldg(p.fwd_ptr + srow + 1);
+              int lo = 0;
+              // s's features are tested against the shared bitmap of N; a hit (rare: |s & N| is small) finds
+              // its q by a binary search of the row's runs (ascending features) from the previous hit on
+              for (int64_t e = e0; e < e1; e += 4) {
+                uint32_t fs[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) fs[j] = e + j < e1 ? (uint32_t)__ldg(p.fwd_idx + e + j) : 0xFFFFFFFFu;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const uint32_t f = fs[j];
+                  if (f == 0xFFFFFFFFu || f >= (uint32_t)p.d || !((s_nbits[f >> 5] >> (f & 31u)) & 1u)) continue;
+                  int hi = nruns;  // lower bound of f in runs [lo, nruns): f is a feature of r, so it is found
+                  while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if ((__ldg(p.runs_f + run_base + mid) & 0xFFFFFFu) < f) lo = mid + 1; else hi = mid;
+                  }
+                  add += (uint32_t)__ldg(p.runs_q + run_base + lo) * (p.fwd_val ? (uint32_t)__ldg(p.fwd_val + e + j) : 1u);
+                  ++lo;
+                }
+              }
+              ++n_complete;
+            }
+            return add;
+          };
 #pragma unroll 2
           for (int c = 0; c < cols; c += 128) {
 #pragma unroll
@@ -531,10 +609,18 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
                 const uint4 x = lds_v4(a);
                 sts_v4_zero(a);
                 const uint32_t mx = max(max(x.x, x.y), max(x.z, x.w));
-                if (__any_sync(0xffffffffu, mx >= t32[b])) {
+                if (__any_sync(0xffffffffu, PRUNE ? (mx != 0u && mx + un >= t32[b]) : mx >= t32[b])) {
                   th[b] = row_theta(b);
                   const uint32_t g0 = gbase + (uint32_t)(cbase + c + lane * 4);
-                  const uint32_t xv[4] = {x.x, x.y, x.z, x.w};
+                  uint32_t xv[4] = {x.x, x.y, x.z, x.w};
+                  if constexpr (PRUNE) {
+                    if (un) {
+                      const uint32_t tc = t32_of(th[b]);
+#pragma unroll
+                      for (int j = 0; j < 4; ++j)
+                        if (xv[j] != 0u && xv[j] + un >= tc) xv[j] += complete((uint32_t)(cbase + c + lane * 4 + j));
+                    }
+                  }
 #pragma unroll
                   for (int j = 0; j < 4; ++j) {
                     const uint64_t key = xv[j] ? make_key(xv[j], g0 + j) : 0;
@@ -798,10 +884,10 @@ cudaError_t launch_accumulate(const Shape& sh, const QP& p, int sms, cudaStream_
 
 #ifdef KJ_ACCUMULATE_INSTANCES
 namespace {
-template <int B, int KS, bool SINT8, int NW, bool HEADS>
+template <int B, int KS, bool SINT8, int NW, bool HEADS, bool PRUNE = false>
 cudaError_t launch_main4(const QP& p, int sms, cudaStream_t st) {
-  const size_t sm = smem_bytes(B, p.T, p.k, NW, p.head_smem != 0);
-  auto kern = k_accumulate_topk<B, KS, SINT8, NW, HEADS>;
+  const size_t sm = align_up(smem_bytes(B, p.T, p.k, NW, p.head_smem != 0), 16) + (PRUNE ? 4 * (size_t)p.prune_words : 0);
+  auto kern = k_accumulate_topk<B, KS, SINT8, NW, HEADS, PRUNE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   int per_sm = 1;
@@ -817,6 +903,9 @@ template <int B, int KS, int NW>
 cudaError_t launch_main(const QP& p, int sms, cudaStream_t st) {
   if constexpr (B * KS <= 24 && B <= NW) {
     if constexpr (B == 1 && NW == 4) {  // the auto shape of indexes without head features
+      if (p.prune_suf)  // pruned queries (a6)
+        return p.vals ? launch_main4<B, KS, true, NW, false, true>(p, sms, st)
+                      : launch_main4<B, KS, false, NW, false, true>(p, sms, st);
       if (!p.head_smem)
         return p.vals ? launch_main4<B, KS, true, NW, false>(p, sms, st) : launch_main4<B, KS, false, NW, false>(p, sms, st);
     }

@@ -32,9 +32,11 @@ __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a -
 struct IndexLayout {
   int64_t n_tiles = 0, n_off = 0, unit_cap = 0;
   size_t off_at = 0, df_at = 0, head_slot_at = 0, head_feat_at = 0, head_cols_at = 0, ids_at = 0, vals_at = 0,
-         total = 0;
+         fwd_ptr_at = 0, fwd_idx_at = 0, fwd_val_at = 0, fmax_at = 0, total = 0;
 };
-bool index_layout(const knnjoin_csr* S, int32_t d, int32_t tile, IndexLayout* L);
+// prune: also reserve S's forward rows and (INT8 S) the per-feature maximum weight (pruned queries, a6)
+bool index_layout(const knnjoin_csr* S, int32_t d, int32_t tile, bool prune, IndexLayout* L);
+constexpr float kDefaultPruneAlpha = 0.25f;
 int32_t resolve_tile(const knnjoin_options* opt);
 
 // per-row score scale: sigma[r] = 2^30 / (sum_d r_d * smax) for FP32 R,
@@ -65,5 +67,12 @@ struct knnjoin_index {
   const uint32_t* head_cols = nullptr; // [n_tiles * tile] bit i: S row has head feature head_feat[i]
   const uint16_t* ids = nullptr;       // [unit_cap*8] local S ids (< tile); padding = tile + (u mod 32)
   const uint8_t* vals = nullptr;       // [unit_cap*8] INT8 S weights (nullptr for BINARY S)
+  // pruned mode (options.prune = 1): forward rows of S (local row ids) and per-feature max weight
+  int32_t prune = 0;
+  float alpha = 0.0f;                  // default alpha of pruned queries
+  const int64_t* fwd_ptr = nullptr;    // [n_s + 1]
+  const int32_t* fwd_idx = nullptr;    // [nnz] features, ascending per row
+  const uint8_t* fwd_val = nullptr;    // [nnz] INT8 S weights (nullptr for BINARY S)
+  const uint32_t* fmax = nullptr;      // [d] largest weight of each feature (nullptr for BINARY S: 1)
   size_t storage_bytes = 0;
 };

@@ -43,7 +43,7 @@ int32_t resolve_tile(const knnjoin_options* opt) {
   return t;
 }
 
-bool index_layout(const knnjoin_csr* S, int32_t d, int32_t tile, IndexLayout* L) {
+bool index_layout(const knnjoin_csr* S, int32_t d, int32_t tile, bool prune, IndexLayout* L) {
   if (!S || d <= 0 || tile <= 0 || S->n_rows < 0 || S->nnz < 0) return false;
   L->n_tiles = (S->n_rows + tile - 1) / tile;
   L->n_off = (int64_t)d * (L->n_tiles + 1) + 1;
@@ -65,6 +65,17 @@ bool index_layout(const knnjoin_csr* S, int32_t d, int32_t tile, IndexLayout* L)
   at = align_up(at + 16 * (size_t)L->unit_cap, 256);
   L->vals_at = at;
   if (S->dtype == KNNJOIN_INT8) at = align_up(at + 8 * (size_t)L->unit_cap, 256);
+  L->fwd_ptr_at = L->fwd_idx_at = L->fwd_val_at = L->fmax_at = at;
+  if (prune) {
+    L->fwd_ptr_at = at;
+    at = align_up(at + sizeof(int64_t) * (size_t)(S->n_rows + 1), 256);
+    L->fwd_idx_at = at;
+    at = align_up(at + sizeof(int32_t) * (size_t)S->nnz, 256);
+    L->fwd_val_at = at;
+    if (S->dtype == KNNJOIN_INT8) at = align_up(at + (size_t)S->nnz, 256);
+    L->fmax_at = at;
+    if (S->dtype == KNNJOIN_INT8) at = align_up(at + sizeof(uint32_t) * (size_t)d, 256);
+  }
   L->total = at;
   return true;
 }
@@ -119,7 +130,11 @@ bool check_build_args(const knnjoin_csr* S, int32_t d, const knnjoin_options* op
   if (S->nnz >= ((int64_t)1 << 31)) { set_error("nnz(S) must be < 2^31 per index (shard S)"); return false; }
   *tile = resolve_tile(opt);
   if (*tile < 0) { set_error("tile must be a multiple of %d in [%d, %d]", kTileQuantum, kTileQuantum, kMaxTile); return false; }
-  if (opt && (opt->prune != 0)) { set_error("pruned mode is not available in this build (options.prune must be 0)"); return false; }
+  if (opt && opt->prune != 0 && opt->prune != 1) { set_error("options.prune must be 0 or 1"); return false; }
+  if (opt && (!(opt->alpha >= 0.0f && opt->alpha <= 1.0f) || (opt->prune == 0 && opt->alpha != 0.0f))) {
+    set_error("options.alpha must be in [0, 1] (0 = default), and 0 when prune = 0");
+    return false;
+  }
   if (opt && opt->head_max > kMaxHead) { set_error("head_max must be <= %d", kMaxHead); return false; }
   if ((int64_t)d * ((S->n_rows + *tile - 1) / *tile + 1) + 1 >= ((int64_t)1 << 31)) {
     set_error("d * (n_tiles+1) too large for 32-bit slice keys; shard S or raise the tile width");
@@ -399,11 +414,22 @@ __global__ void k_head_cols(const int64_t* __restrict__ indptr, const int32_t* _
   if (lane == 0) cols[row] = w;
 }
 
+// pruned mode, INT8 S: the largest weight of every feature (an upper bound of s[d] for the pruning bound
+// c_d = q_r[d] * maxweight(d))
+__global__ void k_fmax(const int32_t* __restrict__ indices, const int8_t* __restrict__ values, int64_t nnz, int32_t d,
+                       uint32_t* __restrict__ fmax) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nnz) return;
+  const int32_t f = indices[i];
+  if (f >= 0 && f < d) atomicMax(&fmax[f], (uint32_t)(uint8_t)values[i]);
+}
+
 }  // namespace
 
 // minimum df of a head feature (0xFFFFFFFF = no heads); BINARY S only
 uint32_t head_min_df(const knnjoin_csr* S, const knnjoin_options* opt) {
   if (S->dtype != KNNJOIN_BINARY || S->n_rows == 0) return 0xFFFFFFFFu;
+  if (opt && opt->prune) return 0xFFFFFFFFu;  // pruned mode runs the head-free one-row kernel
   float dens = opt ? opt->head_density : 0.0f;
   if (dens < 0.0f) return 0xFFFFFFFFu;
   if (dens == 0.0f) dens = kDefaultHeadDensity;
@@ -420,7 +446,7 @@ KJ_API size_t knnjoin_index_bytes(const knnjoin_csr* S, int32_t d, const knnjoin
   int32_t tile;
   if (!check_build_args(S, d, opt, &tile)) return 0;
   IndexLayout L;
-  if (!index_layout(S, d, tile, &L)) { set_error("bad index layout arguments"); return 0; }
+  if (!index_layout(S, d, tile, opt && opt->prune, &L)) { set_error("bad index layout arguments"); return 0; }
   return L.total;
 }
 
@@ -429,7 +455,7 @@ KJ_API size_t knnjoin_build_workspace_bytes(const knnjoin_csr* S, int32_t d, con
   if (!check_build_args(S, d, opt, &tile)) return 0;
   IndexLayout L;
   BuildWs W;
-  if (!index_layout(S, d, tile, &L) || !build_ws_layout(S, d, L, &W)) { set_error("workspace sizing failed"); return 0; }
+  if (!index_layout(S, d, tile, opt && opt->prune, &L) || !build_ws_layout(S, d, L, &W)) { set_error("workspace sizing failed"); return 0; }
   return W.total;
 }
 
@@ -450,7 +476,7 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   if (S->dtype == KNNJOIN_INT8 && S->nnz > 0 && !S->values) { set_error("INT8 S needs values"); return KNNJOIN_ERR_ARG; }
   IndexLayout L;
   BuildWs W;
-  if (!index_layout(S, d, tile, &L) || !build_ws_layout(S, d, L, &W)) { set_error("layout failed"); return KNNJOIN_ERR_ARG; }
+  if (!index_layout(S, d, tile, opt && opt->prune, &L) || !build_ws_layout(S, d, L, &W)) { set_error("layout failed"); return KNNJOIN_ERR_ARG; }
   if (!storage || storage_bytes < L.total) { set_error("index storage %zu < %zu bytes", storage_bytes, L.total); return KNNJOIN_ERR_WORKSPACE; }
   if (!workspace || workspace_bytes < W.total) { set_error("build workspace %zu < %zu bytes", workspace_bytes, W.total); return KNNJOIN_ERR_WORKSPACE; }
   if (((uintptr_t)storage & 255) || ((uintptr_t)workspace & 255)) { set_error("storage and workspace must be 256-byte aligned"); return KNNJOIN_ERR_ARG; }
@@ -525,6 +551,34 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
       if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_head_cols");
     }
   }
+  const bool prune = opt && opt->prune;
+  int64_t* fwd_ptr = nullptr;
+  int32_t* fwd_idx = nullptr;
+  uint8_t* fwd_val = nullptr;
+  uint32_t* fmax = nullptr;
+  if (prune) {  // forward rows for the exact completions of pruned queries (a6)
+    fwd_ptr = (int64_t*)(sb + L.fwd_ptr_at);
+    fwd_idx = (int32_t*)(sb + L.fwd_idx_at);
+    if (S->n_rows > 0 &&
+        (e = cudaMemcpyAsync(fwd_ptr, S->indptr, 8 * (size_t)(S->n_rows + 1), cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+      return cuda_fail(e, "copy forward indptr");
+    if (S->n_rows == 0 && (e = cudaMemsetAsync(fwd_ptr, 0, 8, st)) != cudaSuccess) return cuda_fail(e, "memset indptr");
+    if (S->nnz > 0 &&
+        (e = cudaMemcpyAsync(fwd_idx, S->indices, 4 * (size_t)S->nnz, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+      return cuda_fail(e, "copy forward indices");
+    if (S->dtype == KNNJOIN_INT8) {
+      fwd_val = (uint8_t*)(sb + L.fwd_val_at);
+      fmax = (uint32_t*)(sb + L.fmax_at);
+      if (S->nnz > 0 &&
+          (e = cudaMemcpyAsync(fwd_val, S->values, (size_t)S->nnz, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+        return cuda_fail(e, "copy forward values");
+      if ((e = cudaMemsetAsync(fmax, 0, 4 * (size_t)d, st)) != cudaSuccess) return cuda_fail(e, "memset fmax");
+      if (S->nnz > 0) {
+        k_fmax<<<gnnz, 256, 0, st>>>(S->indices, (const int8_t*)S->values, S->nnz, d, fmax);
+        if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_fmax");
+      }
+    }
+  }
   knnjoin_index* h = new (std::nothrow) knnjoin_index();
   if (!h) { set_error("host allocation failed"); return KNNJOIN_ERR_ARG; }
   h->n_s = S->n_rows;
@@ -537,6 +591,7 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   h->s_dtype = S->dtype;
   h->head_min_df = min_df;
   h->head_max = head_max;
+  if (head_max == 0) h->n_head_host = 0;  // no head features: known without reading the device
   h->off = off;
   h->df = df;
   h->head_slot = head_slot;
@@ -544,6 +599,12 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   h->head_cols = head_cols;
   h->ids = ids;
   h->vals = vals;
+  h->prune = prune ? 1 : 0;
+  h->alpha = prune ? (opt->alpha > 0.0f ? opt->alpha : kDefaultPruneAlpha) : 0.0f;
+  h->fwd_ptr = fwd_ptr;
+  h->fwd_idx = fwd_idx;
+  h->fwd_val = fwd_val;
+  h->fmax = fmax;
   h->storage_bytes = L.total;
   *out = h;
   return KNNJOIN_OK;
@@ -562,6 +623,8 @@ KJ_API knnjoin_status knnjoin_index_stats(const knnjoin_index* idx, knnjoin_inde
   out->s_dtype = idx->s_dtype;
   out->head_min_df = idx->head_min_df == 0xFFFFFFFFu ? -1 : (int64_t)idx->head_min_df;
   out->head_max = idx->head_max;
+  out->prune = idx->prune;
+  out->alpha = idx->alpha;
   return KNNJOIN_OK;
 }
 

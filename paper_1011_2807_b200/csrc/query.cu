@@ -242,8 +242,63 @@ __global__ void __launch_bounds__(kRunThreads) k_build_runs(const int64_t* __res
 // ------------------------------------------------------------------------------------ host dispatch
 struct QueryWs {
   size_t sigma_at, inv_at, runs_f_at, runs_q_at, nruns_at, counter_at, state_at, done_at, wkey_at, wkey2_at,
-      perm_at, perm2_at, rlen_at, rbase_at, cub_at, cub_bytes, part_at, part_bytes, total;
+      perm_at, perm2_at, rlen_at, rbase_at, cub_at, cub_bytes, part_at, part_bytes, prune_at, total;
 };
+
+// a6 (pruned queries, one row per batch): per run i of a row, prune_suf[i] = the sum of c_j = q_j * maxweight(f_j)
+// over the runs j at or after i in the order (c descending, run index ascending) -- the row's features sorted
+// by their bound, suffix sums.  The non-essential set of a tile is {i : prune_suf[i] <= budget}: a suffix of
+// that order whose bounds sum to at most the budget.  One CTA per row: block radix sort of (c, -i) ascending,
+// whose inclusive prefix sums are exactly those suffix sums.  Rows with more runs than the sort holds keep every
+// feature essential (prune_suf = max).
+constexpr int kPruneThreads = 128, kPruneItems = 16;
+__global__ void __launch_bounds__(kPruneThreads) k_prune_prep(const int64_t* __restrict__ indptr,
+                                                              const int64_t* __restrict__ rbase,
+                                                              const uint32_t* __restrict__ runs_f,
+                                                              const int32_t* __restrict__ runs_q,
+                                                              const uint32_t* __restrict__ batch_nruns,
+                                                              const uint32_t* __restrict__ fmax,
+                                                              uint32_t* __restrict__ prune_suf) {
+  using BRS = cub::BlockRadixSort<uint64_t, kPruneThreads, kPruneItems, int32_t>;
+  using BScan = cub::BlockScan<uint64_t, kPruneThreads>;
+  __shared__ union {
+    typename BRS::TempStorage sort;
+    typename BScan::TempStorage scan;
+  } sm;
+  constexpr int kCapRuns = kPruneThreads * kPruneItems;  // 2048 = 2^11: the run index fits 11 key bits
+  const int64_t batch = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int64_t base = rbase ? rbase[batch] : indptr[batch];
+  const int n = (int)batch_nruns[batch];
+  if (n > kCapRuns) {
+    for (int i = tid; i < n; i += kPruneThreads) prune_suf[base + i] = 0xFFFFFFFFu;
+    return;
+  }
+  constexpr uint64_t kInvalid = ~0ull;
+  uint64_t key[kPruneItems];
+  int32_t idx[kPruneItems];
+#pragma unroll
+  for (int it = 0; it < kPruneItems; ++it) {
+    const int i = tid * kPruneItems + it;
+    key[it] = kInvalid;
+    idx[it] = i;
+    if (i < n) {
+      const uint32_t f = runs_f[base + i] & 0xFFFFFFu;
+      uint64_t c = (uint64_t)(uint32_t)runs_q[base + i] * (fmax ? (uint64_t)fmax[f] : 1ull);
+      if (c > 0xFFFFFFFFull) c = 0xFFFFFFFFull;
+      key[it] = (c << 11) | (uint64_t)(kCapRuns - 1 - i);  // ascending (c, -i) = reverse of (c desc, i asc)
+    }
+  }
+  BRS(sm.sort).Sort(key, idx, 0, 44);
+  __syncthreads();
+  uint64_t c[kPruneItems];
+#pragma unroll
+  for (int it = 0; it < kPruneItems; ++it) c[it] = key[it] == kInvalid ? 0ull : key[it] >> 11;
+  BScan(sm.scan).InclusiveSum(c, c);
+#pragma unroll
+  for (int it = 0; it < kPruneItems; ++it)
+    if (key[it] != kInvalid) prune_suf[base + idx[it]] = c[it] > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c[it];
+}
 
 bool shape_supported(int B, int NW, int KS) {
   if (B * KS > 24 || B > NW) return false;
@@ -338,6 +393,7 @@ bool query_ws_layout(int64_t n_r, int64_t nnz_r, int B, int NW, int k, int sms, 
   W->part_bytes = n_batches < kSplitWaves * ctas
                       ? 8 * (size_t)k * (size_t)((kSplitWaves * ctas + n_batches) * B) : 0;
   W->part_at = at;    at = align_up(at + W->part_bytes, 256);
+  W->prune_at = at;   at = align_up(at + 4 * (size_t)nnz_r, 256);  // a6 suffix bounds (pruned queries)
   W->total = at;
   return true;
 }
@@ -448,6 +504,17 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
     set_error("integer scores may overflow 32 bits for d = %d", idx->d);
     return KNNJOIN_ERR_UNSUPPORTED;
   }
+  // a6: effective pruning alpha (0 = not pruned)
+  float alpha = 0.0f;
+  if (qopt && qopt->prune_alpha != 0.0f && !idx->prune && qopt->prune_alpha > 0.0f) {
+    set_error("prune_alpha > 0 needs an index built with options.prune = 1");
+    return KNNJOIN_ERR_ARG;
+  }
+  if (qopt && (qopt->prune_alpha > 1.0f || qopt->prune_alpha != qopt->prune_alpha)) {
+    set_error("prune_alpha must be <= 1");
+    return KNNJOIN_ERR_ARG;
+  }
+  if (idx->prune) alpha = (qopt && qopt->prune_alpha != 0.0f) ? (qopt->prune_alpha > 0.0f ? qopt->prune_alpha : 0.0f) : idx->alpha;
   const bool auto_shape = !qopt || (qopt->batch_rows == 0 && qopt->cta_warps == 0);
   if (auto_shape && idx->n_head_host < 0) {
     // first auto-shaped query on this index: read its head count once (4-byte copy; synchronises `stream`)
@@ -470,6 +537,14 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
     set_error("tile range [%lld, %lld) outside [0, %lld]", (long long)qopt->tile_begin, (long long)qopt->tile_end,
               (long long)idx->n_tiles);
     return KNNJOIN_ERR_ARG;
+  }
+  if (alpha > 0.0f && (size_t)((idx->d + 31) / 32) * 4 + smem_bytes(1, idx->tile, k, 4, false) > 200 * 1024) {
+    set_error("pruned queries keep a d-bit map in shared memory: d = %d too large", idx->d);
+    return KNNJOIN_ERR_UNSUPPORTED;
+  }
+  if (alpha > 0.0f && !(sh.B == 1 && sh.NW == 4)) {
+    set_error("pruned queries run one-row 4-warp CTAs (batch_rows 1, cta_warps 4); got %d / %d", sh.B, sh.NW);
+    return KNNJOIN_ERR_UNSUPPORTED;
   }
   const int B = sh.B;
   QueryWs W;
@@ -541,6 +616,13 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
                                                                     idx->d, B, n_batches, sigma, perm, rbase, runs_f, runs_q, nruns, kbits);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_build_runs");
   }
+  uint32_t* prune_suf = nullptr;
+  if (alpha > 0.0f) {
+    prune_suf = (uint32_t*)(wb + W.prune_at);
+    k_prune_prep<<<(unsigned)n_batches, kPruneThreads, 0, st>>>(R->indptr, rbase, runs_f, runs_q, nruns, idx->fmax,
+                                                               prune_suf);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_prune_prep");
+  }
   QP p;
   p.off = idx->off;
   p.ids = idx->ids;
@@ -599,6 +681,13 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
     p.tiles_per_pass = tpp;
     p.n_passes = span > 0 ? (span + tpp - 1) / tpp : 1;  // an empty range still runs one (tile-less) pass
   }
+  p.alpha = alpha;
+  p.prune_suf = prune_suf;
+  p.fwd_ptr = idx->fwd_ptr;
+  p.fwd_idx = idx->fwd_idx;
+  p.fwd_val = idx->fwd_val;
+  p.fmax = idx->fmax;
+  p.prune_words = (idx->d + 31) / 32;
   p.state_keys = state_keys;
   p.pass_done = pass_done;
   p.counters = (unsigned long long*)(qopt ? qopt->counters : nullptr);

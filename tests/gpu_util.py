@@ -9,14 +9,16 @@ TOL = 1e-5  # BASELINE.json north_star: fp32 scores within 1e-5 relative
 
 
 def gpu_join(R, S, k, d=None, tile=0, batch_rows=0, s_id_base=0, want_keys=False, counters=None, head_density=0.0,
-             head_max=0, cta_warps=0, tiles_per_pass=0, row_order=0):
+             head_max=0, cta_warps=0, tiles_per_pass=0, row_order=0, prune=0, alpha=0.0, prune_alpha=0.0):
     import paper_1011_2807_b200 as kj
     d = d or R.d
     dS = kj.DeviceCSR.from_host(S)
     dR = kj.DeviceCSR.from_host(R)
-    idx = kj.knnjoin_build_index(dS, d, s_id_base=s_id_base, tile=tile, head_density=head_density, head_max=head_max)
+    idx = kj.knnjoin_build_index(dS, d, s_id_base=s_id_base, tile=tile, head_density=head_density, head_max=head_max,
+                                 prune=prune, alpha=alpha)
     ids, sc, keys = kj.knnjoin_query(idx, dR, k, want_keys=want_keys, batch_rows=batch_rows, counters=counters,
-                                     cta_warps=cta_warps, tiles_per_pass=tiles_per_pass, row_order=row_order)
+                                     cta_warps=cta_warps, tiles_per_pass=tiles_per_pass, row_order=row_order,
+                                     prune_alpha=prune_alpha)
     torch.cuda.synchronize()
     out = (ids.cpu().numpy().astype(np.int64), sc.cpu().numpy().astype(np.float64))
     if want_keys:

@@ -57,3 +57,48 @@ def test_build_argument_errors(d, tile, dtype, msg):
     opt = b._Options(tile, 0, 0.0, 0.0, 0)
     assert L.knnjoin_index_bytes(ctypes.byref(S), d, ctypes.byref(opt)) == 0
     assert msg in b.knnjoin_last_error()
+
+
+def test_prune_index_bytes_and_argument_errors():
+    """prune = 1 reserves S's forward rows (+ per-feature max weights for INT8 S); bad prune / alpha fail."""
+    import paper_1011_2807_b200._binding as b
+    L = b._lib
+    al = lambda x: (x + 255) // 256 * 256
+    for dt, extra in ((b.BINARY, lambda n, z, d: al(8 * (n + 1)) + al(4 * z)),
+                      (b.INT8, lambda n, z, d: al(8 * (n + 1)) + al(4 * z) + al(z) + al(4 * d))):
+        S = b._CSR(50_000, 1_000_000, 0, 0, 0, dt)
+        base = L.knnjoin_index_bytes(ctypes.byref(S), 10_000, ctypes.byref(b._Options(8192, 0, 0.0, 0.0, 0)))
+        pr = L.knnjoin_index_bytes(ctypes.byref(S), 10_000, ctypes.byref(b._Options(8192, 1, 0.5, 0.0, 0)))
+        assert base > 0 and pr == base + extra(50_000, 1_000_000, 10_000)
+    S = b._CSR(10, 20, 0, 0, 0, b.BINARY)
+    for opt, msg in ((b._Options(8192, 2, 0.0, 0.0, 0), "prune"), (b._Options(8192, 1, 1.5, 0.0, 0), "alpha"),
+                     (b._Options(8192, 0, 0.5, 0.0, 0), "alpha")):
+        assert L.knnjoin_index_bytes(ctypes.byref(S), 100, ctypes.byref(opt)) == 0
+        assert msg in b.knnjoin_last_error()
+
+
+def test_ctypes_structs_match_the_c_header(tmp_path):
+    """The binding's ctypes structures have the C header's sizes and field offsets (compiled with gcc)."""
+    import shutil
+    import subprocess
+    import paper_1011_2807_b200._binding as b
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    structs = {"knnjoin_csr": b._CSR, "knnjoin_options": b._Options, "knnjoin_query_options": b._QueryOptions,
+               "knnjoin_index_info": b._IndexInfo}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "knnjoin.h"', "int main(void) {"]
+    for cname, cls in structs.items():
+        lines.append(f'  printf("{cname} %zu\\n", sizeof({cname}));')
+        for f, _ in cls._fields_:
+            lines.append(f'  printf("{cname}.{f} %zu\\n", offsetof({cname}, {f}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call([cc, "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    got = dict(l.split() for l in subprocess.check_output([str(exe)], text=True).splitlines())
+    for cname, cls in structs.items():
+        assert int(got[cname]) == ctypes.sizeof(cls), cname
+        for f, _ in cls._fields_:
+            assert int(got[f"{cname}.{f}"]) == getattr(cls, f).offset, f"{cname}.{f}"
