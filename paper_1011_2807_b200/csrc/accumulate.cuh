@@ -44,7 +44,7 @@ struct QP {
   unsigned long long* phase;  // [8] cycles per phase (profiling), or nullptr
   // threshold pruning (a6; PRUNE instances only)
   float alpha;               // non-essential budget = min(alpha * theta, theta - 1)
-  const uint32_t* prune_suf; // [runs] per run: sum of c over the runs at or after it in c-descending order
+  const uint2* prune_suf;    // [runs] per run: {sum of c over the runs at or after it in c-descending order, c}
   const int64_t* fwd_ptr;    // [n_s + 1] forward rows of S (local row ids)
   const int32_t* fwd_idx;    // [nnz(S)]
   const uint8_t* fwd_val;    // [nnz(S)] INT8 S weights, or nullptr (BINARY)
@@ -364,11 +364,12 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
               u0[it] = o[0];
               U[it] = o[1] - u0[it];
               if constexpr (PRUNE) {
-                if (__ldg(p.prune_suf + run_base + i) <= budget) {  // non-essential: slice not loaded
+                const uint2 sc = __ldg(p.prune_suf + run_base + i);
+                if (sc.x <= budget) {  // non-essential: slice not loaded
                   const uint32_t f = fm[it] & 0xFFFFFFu;
                   atomicOr(&s_nbits[f >> 5], 1u << (f & 31u));
                   if (U[it] > 0) {
-                    un_mine += (uint32_t)__ldg(p.runs_q + run_base + i) * (p.fmax ? __ldg(p.fmax + f) : 1u);
+                    un_mine += sc.y;
                     n_skipped += U[it];
                   }
                   U[it] = 0;

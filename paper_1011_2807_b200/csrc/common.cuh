@@ -75,4 +75,5 @@ struct knnjoin_index {
   const uint8_t* fwd_val = nullptr;    // [nnz] INT8 S weights (nullptr for BINARY S)
   const uint32_t* fmax = nullptr;      // [d] largest weight of each feature (nullptr for BINARY S: 1)
   size_t storage_bytes = 0;
+  size_t fwd_bytes = 0;                // part of storage_bytes holding the forward rows (not swept per tile)
 };

@@ -606,6 +606,7 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   h->fwd_val = fwd_val;
   h->fmax = fmax;
   h->storage_bytes = L.total;
+  h->fwd_bytes = prune ? L.total - L.fwd_ptr_at : 0;
   *out = h;
   return KNNJOIN_OK;
 }

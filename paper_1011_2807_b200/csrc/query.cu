@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(kPruneThreads) k_prune_prep(const int64_t* __r
                                                               const int32_t* __restrict__ runs_q,
                                                               const uint32_t* __restrict__ batch_nruns,
                                                               const uint32_t* __restrict__ fmax,
-                                                              uint32_t* __restrict__ prune_suf) {
+                                                              uint2* __restrict__ prune_suf) {
   using BRS = cub::BlockRadixSort<uint64_t, kPruneThreads, kPruneItems, int32_t>;
   using BScan = cub::BlockScan<uint64_t, kPruneThreads>;
   __shared__ union {
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(kPruneThreads) k_prune_prep(const int64_t* __r
   const int64_t base = rbase ? rbase[batch] : indptr[batch];
   const int n = (int)batch_nruns[batch];
   if (n > kCapRuns) {
-    for (int i = tid; i < n; i += kPruneThreads) prune_suf[base + i] = 0xFFFFFFFFu;
+    for (int i = tid; i < n; i += kPruneThreads) prune_suf[base + i] = make_uint2(0xFFFFFFFFu, 0u);
     return;
   }
   constexpr uint64_t kInvalid = ~0ull;
@@ -297,7 +297,9 @@ __global__ void __launch_bounds__(kPruneThreads) k_prune_prep(const int64_t* __r
   BScan(sm.scan).InclusiveSum(c, c);
 #pragma unroll
   for (int it = 0; it < kPruneItems; ++it)
-    if (key[it] != kInvalid) prune_suf[base + idx[it]] = c[it] > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c[it];
+    if (key[it] != kInvalid)
+      prune_suf[base + idx[it]] = make_uint2(c[it] > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c[it],
+                                             (uint32_t)(key[it] >> 11));
 }
 
 bool shape_supported(int B, int NW, int KS) {
@@ -393,7 +395,7 @@ bool query_ws_layout(int64_t n_r, int64_t nnz_r, int B, int NW, int k, int sms, 
   W->part_bytes = n_batches < kSplitWaves * ctas
                       ? 8 * (size_t)k * (size_t)((kSplitWaves * ctas + n_batches) * B) : 0;
   W->part_at = at;    at = align_up(at + W->part_bytes, 256);
-  W->prune_at = at;   at = align_up(at + 4 * (size_t)nnz_r, 256);  // a6 suffix bounds (pruned queries)
+  W->prune_at = at;   at = align_up(at + 8 * (size_t)nnz_r, 256);  // a6 {suffix bound, c} per run (pruned queries)
   W->total = at;
   return true;
 }
@@ -616,9 +618,9 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
                                                                     idx->d, B, n_batches, sigma, perm, rbase, runs_f, runs_q, nruns, kbits);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_build_runs");
   }
-  uint32_t* prune_suf = nullptr;
+  uint2* prune_suf = nullptr;
   if (alpha > 0.0f) {
-    prune_suf = (uint32_t*)(wb + W.prune_at);
+    prune_suf = (uint2*)(wb + W.prune_at);
     k_prune_prep<<<(unsigned)n_batches, kPruneThreads, 0, st>>>(R->indptr, rbase, runs_f, runs_q, nruns, idx->fmax,
                                                                prune_suf);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_prune_prep");
@@ -657,7 +659,8 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
     int64_t tpp = qopt ? qopt->tiles_per_pass : 0;
     if (tpp <= 0) {
-      const double per_tile = (double)idx->storage_bytes / (double)(idx->n_tiles > 0 ? idx->n_tiles : 1);
+      const double per_tile =
+          (double)(idx->storage_bytes - idx->fwd_bytes) / (double)(idx->n_tiles > 0 ? idx->n_tiles : 1);
       tpp = (int64_t)((double)(l2 > 0 ? l2 : (96 << 20)) / 3.0 / (per_tile > 1.0 ? per_tile : 1.0));
       if (tpp < 1) tpp = 1;
     }
