@@ -72,6 +72,8 @@ typedef struct {
  *   every s whose partial score plus sum_{d in N, slice non-empty} c_d reaches theta.  An s that the
  *   skipped slices alone could reach has score < theta and cannot enter.  Results are identical to the
  *   unpruned query; only the work changes.  prune = 0: alpha must be 0.
+ * forward: NULL, or (prune = 1) a CSR with S's row count whose rows are kept as the forward rows instead of
+ *   S's own (f1, IIIB-literal: the residual rows s' of knnjoin_iiib_split, completed by residual queries).
  * head_density / head_max: "head features" (BINARY S only).  Up to head_max (0 = 32, at most 32) of the
  *   most frequent features with df >= head_density * |S| (0 = default 1/8, negative = no head features) are
  *   not stored as id lists: each S row gets one 32-bit word of head-feature bits.  During the top-k scan the
@@ -85,6 +87,7 @@ typedef struct {
   float alpha;
   float head_density;
   int32_t head_max;
+  const knnjoin_csr* forward;
 } knnjoin_options;
 
 /* Query options (all optional; pass NULL for defaults).
@@ -132,7 +135,12 @@ typedef struct {
  *              alpha, in (0, 1] = this alpha, < 0 = off.  On an index built without prune it must be 0 or
  *              negative.  Pruned queries run the one-row 4-warp shape (batch_rows / cta_warps must be 0 or
  *              1 / 4).  counters [2] then counts the 16-byte posting units (8 postings, padding included) whose
- *              loads were skipped, and [3] the exact completions ((row, S row) pairs). */
+ *              loads were skipped, and [3] the exact completions ((row, S row) pairs).
+ *  residual:   1 = f1 (IIIB-literal, Alg. 4 lines 15-24): the index holds only the indexed
+ *              parts s'' of its S rows and its forward rows are the residual parts s' (knnjoin_iiib_split):
+ *              every s with a non-zero partial score is completed with dot(r, s') (line 21) before the
+ *              candidate test.  Needs an index built with prune = 1; not combinable with prune_alpha > 0.
+ *              counters [3] counts the completions. */
 typedef struct {
   int32_t batch_rows;
   int64_t* counters;
@@ -147,6 +155,7 @@ typedef struct {
   const uint64_t* resume_keys;
   const uint64_t* theta_in;
   float prune_alpha;
+  int32_t residual;
 } knnjoin_query_options;
 
 typedef struct knnjoin_index knnjoin_index; /* opaque HOST handle; borrows the caller's index storage */
@@ -228,6 +237,41 @@ size_t knnjoin_merge_workspace_bytes(const knnjoin_csr* R);
 knnjoin_status knnjoin_merge(const uint64_t* keys, int32_t P, const knnjoin_csr* R, int32_t d,
                              knnjoin_dtype s_dtype, int32_t k, uint64_t* out_keys, int32_t* out_ids, float* out_scores, void* workspace,
                              size_t workspace_bytes, void* stream);
+
+/* ---- f1: IIIB-literal (Alg. 4) building blocks --------------------------------------
+ * The paper's improved algorithm per (R block, S block): dimensions reordered by their non-zero count in the
+ * R block (descending; ties by dimension; dimensions absent from the block last), maxWeight_d = the largest
+ * weight of dimension d in the R block, MinPruneScore = min over the block's rows of pruneScore(r) (the k-th
+ * score so far, 0 while fewer than k are held).  Each s of the S block is walked in that order with
+ * t += maxWeight_d * w; from the first feature at which t > MinPruneScore on, its features are indexed (s''),
+ * the others stay in s'.  The S block is then indexed from s'' (prune = 1, forward = s') and queried with
+ * residual = 1, which adds dot(r, s') to every touched s (Theorem 1: an s sharing no indexed
+ * feature with r has dot(r, s) <= MinPruneScore <= pruneScore(r) and cannot enter).  R is one block here. */
+
+/* Bytes of the device profile of R (maxWeight, dimension order, sort scratch). */
+size_t knnjoin_iiib_profile_bytes(const knnjoin_csr* R, int32_t d);
+
+/* Alg. 4 lines 6-7 over all of R: writes the profile into `profile` (device, >= knnjoin_iiib_profile_bytes). */
+knnjoin_status knnjoin_iiib_profile(const knnjoin_csr* R, int32_t d, void* profile, size_t profile_bytes, void* stream);
+
+/* MinPruneScore of R from the keys of the S blocks done so far (keys: [n_rows][k] as knnjoin_query writes them,
+ * or NULL before the first block -> 0), written to out2 (device double[2]) as {min_r kth_score(r) (real
+ * units), max_r 1/sigma_r}.  For FP32 R (per-row fixed-point scores) knnjoin_iiib_split lowers the threshold
+ * of an s by (sum of its weights + 1) * out2[1] so that rounding can never let an unindexed-only s enter. */
+knnjoin_status knnjoin_iiib_threshold(const uint64_t* keys, const knnjoin_csr* R, int32_t d, knnjoin_dtype s_dtype,
+                                      int32_t k, double* out2, void* workspace, size_t workspace_bytes, void* stream);
+size_t knnjoin_iiib_threshold_workspace_bytes(const knnjoin_csr* R);
+
+/* Alg. 4 lines 8-14 on the S block: split every row of S into the indexed part (out_idx) and the residual
+ * part (out_res), both CSRs with S's row count, features ascending, INT8 values carried (out_*_values NULL
+ * for BINARY S); the arrays of each need room for nnz(S) entries and n_rows + 1 indptr entries.  Their nnz
+ * are known on the device only (indptr[n_rows]).  threshold: device double[2] from knnjoin_iiib_threshold;
+ * r_integer: 1 when R is BINARY/INT8 (exact scores: no rounding margin). */
+knnjoin_status knnjoin_iiib_split(const knnjoin_csr* S, int32_t d, const void* profile, const double* threshold,
+                                  int32_t r_integer, int64_t* idx_indptr, int32_t* idx_indices, int8_t* idx_values,
+                                  int64_t* res_indptr, int32_t* res_indices, int8_t* res_values, void* workspace,
+                                  size_t workspace_bytes, void* stream);
+size_t knnjoin_iiib_split_workspace_bytes(const knnjoin_csr* S);
 
 /* ---- validation (not on the hot path) ------------------------------------------------------------- */
 

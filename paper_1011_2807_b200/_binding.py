@@ -32,7 +32,7 @@ class _CSR(ctypes.Structure):
 
 class _Options(ctypes.Structure):
     _fields_ = [("tile", ctypes.c_int32), ("prune", ctypes.c_int32), ("alpha", ctypes.c_float),
-                ("head_density", ctypes.c_float), ("head_max", ctypes.c_int32)]
+                ("head_density", ctypes.c_float), ("head_max", ctypes.c_int32), ("forward", ctypes.c_void_p)]
 
 
 class _QueryOptions(ctypes.Structure):
@@ -40,7 +40,7 @@ class _QueryOptions(ctypes.Structure):
                 ("ev_end", ctypes.c_void_p), ("phase_cycles", ctypes.c_void_p), ("cta_warps", ctypes.c_int32),
                 ("tiles_per_pass", ctypes.c_int32), ("row_order", ctypes.c_int32), ("tile_begin", ctypes.c_int64),
                 ("tile_end", ctypes.c_int64), ("resume_keys", ctypes.c_void_p), ("theta_in", ctypes.c_void_p),
-                ("prune_alpha", ctypes.c_float)]
+                ("prune_alpha", ctypes.c_float), ("residual", ctypes.c_int32)]
 
 
 class _IndexInfo(ctypes.Structure):
@@ -85,6 +85,20 @@ def _load():
     L.knnjoin_merge.restype = c.c_int
     L.knnjoin_validate_csr.argtypes = [P(_CSR), c.c_int32, c.c_void_p, P(c.c_int64)]
     L.knnjoin_validate_csr.restype = c.c_int
+    L.knnjoin_iiib_profile_bytes.argtypes = [P(_CSR), c.c_int32]
+    L.knnjoin_iiib_profile_bytes.restype = c.c_size_t
+    L.knnjoin_iiib_profile.argtypes = [P(_CSR), c.c_int32, c.c_void_p, c.c_size_t, c.c_void_p]
+    L.knnjoin_iiib_profile.restype = c.c_int
+    L.knnjoin_iiib_threshold_workspace_bytes.argtypes = [P(_CSR)]
+    L.knnjoin_iiib_threshold_workspace_bytes.restype = c.c_size_t
+    L.knnjoin_iiib_threshold.argtypes = [c.c_void_p, P(_CSR), c.c_int32, c.c_int, c.c_int32, c.c_void_p, c.c_void_p,
+                                         c.c_size_t, c.c_void_p]
+    L.knnjoin_iiib_threshold.restype = c.c_int
+    L.knnjoin_iiib_split_workspace_bytes.argtypes = [P(_CSR)]
+    L.knnjoin_iiib_split_workspace_bytes.restype = c.c_size_t
+    L.knnjoin_iiib_split.argtypes = [P(_CSR), c.c_int32, c.c_void_p, c.c_void_p, c.c_int32, c.c_void_p, c.c_void_p,
+                                     c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_size_t, c.c_void_p]
+    L.knnjoin_iiib_split.restype = c.c_int
     L.knnjoin_last_error.argtypes = []
     L.knnjoin_last_error.restype = c.c_char_p
     L.knnjoin_version.argtypes = []
@@ -96,7 +110,9 @@ _lib = _load()
 
 EXPORTS = ["knnjoin_index_bytes", "knnjoin_build_workspace_bytes", "knnjoin_build_index", "knnjoin_index_stats",
            "knnjoin_free_index", "knnjoin_query_workspace_bytes", "knnjoin_query", "knnjoin_merge_workspace_bytes",
-           "knnjoin_merge", "knnjoin_validate_csr", "knnjoin_last_error", "knnjoin_version"]
+           "knnjoin_merge", "knnjoin_validate_csr", "knnjoin_last_error", "knnjoin_version",
+           "knnjoin_iiib_profile_bytes", "knnjoin_iiib_profile", "knnjoin_iiib_threshold_workspace_bytes",
+           "knnjoin_iiib_threshold", "knnjoin_iiib_split_workspace_bytes", "knnjoin_iiib_split"]
 
 
 def knnjoin_last_error() -> str:
@@ -187,10 +203,13 @@ def _empty_u8(nbytes: int, device) -> torch.Tensor:
 
 def knnjoin_build_index(S: DeviceCSR, d: int, s_id_base: int = 0, tile: int = 0, stream=None,
                         workspace: torch.Tensor | None = None, head_density: float = 0.0,
-                        head_max: int = 0, prune: int = 0, alpha: float = 0.0) -> Index:
-    """prune=1 keeps S's forward rows for threshold-pruned queries (a6; knnjoin_options.prune / alpha)."""
+                        head_max: int = 0, prune: int = 0, alpha: float = 0.0,
+                        forward: "DeviceCSR | None" = None) -> Index:
+    """prune=1 keeps S's forward rows for threshold-pruned queries (a6; knnjoin_options.prune / alpha), or the
+    rows of `forward` instead (f1: the residual parts s')."""
     cS = S._c()
-    opt = _Options(tile, prune, alpha, head_density, head_max)
+    cF = forward._c() if forward is not None else None
+    opt = _Options(tile, prune, alpha, head_density, head_max, ctypes.addressof(cF) if cF is not None else 0)
     nbytes = _lib.knnjoin_index_bytes(ctypes.byref(cS), d, ctypes.byref(opt))
     if nbytes == 0:
         raise KnnJoinError(1, "knnjoin_index_bytes", knnjoin_last_error())
@@ -220,7 +239,7 @@ def knnjoin_query(index: Index, R: DeviceCSR, k: int, want_keys: bool = False, w
                   workspace: torch.Tensor | None = None, phase_cycles: torch.Tensor | None = None,
                   cta_warps: int = 0, tiles_per_pass: int = 0, row_order: int = 0, tile_range=(0, 0),
                   resume_keys: torch.Tensor | None = None, theta_in: torch.Tensor | None = None,
-                  prune_alpha: float = 0.0):
+                  prune_alpha: float = 0.0, residual: int = 0):
     """Returns (ids int32 [n,k], scores float32 [n,k], keys uint64-as-int64 [n,k] or None).
     tile_range / resume_keys (int64 [n,k]) / theta_in (int64 [n]) / prune_alpha: see knnjoin_query_options."""
     for t, shape in ((resume_keys, (R.n_rows, k)), (theta_in, (R.n_rows,))):
@@ -234,7 +253,7 @@ def knnjoin_query(index: Index, R: DeviceCSR, k: int, want_keys: bool = False, w
                        phase_cycles.data_ptr() if phase_cycles is not None else 0, cta_warps, tiles_per_pass,
                        row_order, tile_range[0], tile_range[1],
                        resume_keys.data_ptr() if resume_keys is not None else 0,
-                       theta_in.data_ptr() if theta_in is not None else 0, prune_alpha)
+                       theta_in.data_ptr() if theta_in is not None else 0, prune_alpha, residual)
     wbytes = _lib.knnjoin_query_workspace_bytes(index.handle, ctypes.byref(cR), k, ctypes.byref(qo))
     if wbytes == 0:
         raise KnnJoinError(1, "knnjoin_query_workspace_bytes", knnjoin_last_error())
@@ -278,3 +297,61 @@ def knnjoin_validate_csr(m: DeviceCSR, d: int, stream=None):
     if st not in (0, 3):
         _check(st, "knnjoin_validate_csr")
     return st, bad.value
+
+
+# ---- f1: IIIB-literal building blocks (knnjoin_iiib_*) -------------------------------------------------------
+
+def knnjoin_iiib_profile(R: DeviceCSR, d: int, stream=None) -> torch.Tensor:
+    """Alg. 4 lines 6-7 over all of R -> opaque device profile (uint8 tensor)."""
+    cR = R._c()
+    nb = _lib.knnjoin_iiib_profile_bytes(ctypes.byref(cR), d)
+    if nb == 0:
+        raise KnnJoinError(1, "knnjoin_iiib_profile_bytes", knnjoin_last_error())
+    prof = _empty_u8(nb, R.indptr.device)
+    _check(_lib.knnjoin_iiib_profile(ctypes.byref(cR), d, prof.data_ptr(), nb, _stream_ptr(stream)),
+           "knnjoin_iiib_profile")
+    return prof
+
+
+def knnjoin_iiib_threshold(keys: torch.Tensor | None, R: DeviceCSR, d: int, s_dtype: int, k: int,
+                           stream=None) -> torch.Tensor:
+    """MinPruneScore from the current keys (None before the first S block) -> device float64[2]."""
+    cR = R._c()
+    wb = _lib.knnjoin_iiib_threshold_workspace_bytes(ctypes.byref(cR))
+    ws = _empty_u8(wb, R.indptr.device)
+    out = torch.empty(2, dtype=torch.float64, device=R.indptr.device)
+    _check(_lib.knnjoin_iiib_threshold(keys.data_ptr() if keys is not None else 0, ctypes.byref(cR), d, s_dtype, k,
+                                       out.data_ptr(), ws.data_ptr(), wb, _stream_ptr(stream)),
+           "knnjoin_iiib_threshold")
+    return out
+
+
+def knnjoin_iiib_split(S: DeviceCSR, d: int, profile: torch.Tensor, threshold: torch.Tensor, r_integer: bool,
+                       rows=None, stream=None):
+    """Alg. 4 lines 8-14 on rows [lo, hi) of S (all if None) -> (indexed s'', residual s') DeviceCSRs.
+    Reads the two nnz back (a 16-byte device-to-host copy that synchronises the stream)."""
+    lo, hi = rows if rows is not None else (0, S.n_rows)
+    n = hi - lo
+    nnz = int(S.nnz)
+    # a row-range view: indptr from row lo on (absolute positions into S's indices / values)
+    cS = _CSR(n, nnz, S.indptr.data_ptr() + 8 * lo, S.indices.data_ptr() if nnz else 0,
+              S.values.data_ptr() if (S.values is not None and nnz) else 0, S.dtype)
+    dev = S.indptr.device
+    cap = max(1, nnz)
+    ip_i = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    ip_r = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    ix_i = torch.empty(cap, dtype=torch.int32, device=dev)
+    ix_r = torch.empty(cap, dtype=torch.int32, device=dev)
+    v_i = torch.empty(cap, dtype=torch.int8, device=dev) if S.dtype == INT8 else None
+    v_r = torch.empty(cap, dtype=torch.int8, device=dev) if S.dtype == INT8 else None
+    wb = _lib.knnjoin_iiib_split_workspace_bytes(ctypes.byref(cS))
+    ws = _empty_u8(wb, dev)
+    _check(_lib.knnjoin_iiib_split(ctypes.byref(cS), d, profile.data_ptr(), threshold.data_ptr(), int(bool(r_integer)),
+                                   ip_i.data_ptr(), ix_i.data_ptr(), v_i.data_ptr() if v_i is not None else 0,
+                                   ip_r.data_ptr(), ix_r.data_ptr(), v_r.data_ptr() if v_r is not None else 0,
+                                   ws.data_ptr(), wb, _stream_ptr(stream)), "knnjoin_iiib_split")
+    ends = torch.stack([ip_i[n], ip_r[n]]).cpu()
+    ni, nr = int(ends[0]), int(ends[1])
+    idx = DeviceCSR(ip_i, ix_i[:ni], v_i[:ni] if v_i is not None else None, S.dtype)
+    res = DeviceCSR(ip_r, ix_r[:nr], v_r[:nr] if v_r is not None else None, S.dtype)
+    return idx, res

@@ -50,6 +50,8 @@ struct QP {
   const uint8_t* fwd_val;    // [nnz(S)] INT8 S weights, or nullptr (BINARY)
   const uint32_t* fmax;      // [d] largest S weight per feature, or nullptr (BINARY: 1)
   int32_t prune_words;       // (d + 31) / 32: shared bitmap of the row's non-essential features
+  int32_t residual;          // f1 (IIIB-literal): every run is "non-essential" for the completion (its bit is
+                             // set) but its slice is loaded; every touched s is completed with dot(r, s')
   // out
   uint64_t* out_keys;
   int32_t* out_ids;
@@ -364,8 +366,11 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
               u0[it] = o[0];
               U[it] = o[1] - u0[it];
               if constexpr (PRUNE) {
-                const uint2 sc = __ldg(p.prune_suf + run_base + i);
-                if (sc.x <= budget) {  // non-essential: slice not loaded
+                const uint2 sc = p.residual ? make_uint2(0xFFFFFFFFu, 0u) : __ldg(p.prune_suf + run_base + i);
+                if (p.residual) {  // f1: r's feature set for dot(r, s'), slices all loaded
+                  const uint32_t f = fm[it] & 0xFFFFFFu;
+                  atomicOr(&s_nbits[f >> 5], 1u << (f & 31u));
+                } else if (sc.x <= budget) {  // non-essential: slice not loaded
                   const uint32_t f = fm[it] & 0xFFFFFFu;
                   atomicOr(&s_nbits[f >> 5], 1u << (f & 31u));
                   if (U[it] > 0) {
@@ -379,7 +384,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
             pk[it] = ((uint64_t)(U[it] > 0) << 32) | U[it];
             mine += pk[it];
           }
-          if (PRUNE && c0 == 0 && tid == 0) s_misc[4] = 0;  // U_N of this tile (read after the accumulate)
+          // U_N of this tile (read after the accumulate); f1: 2^31 > any score, i.e. complete every touched s
+          if (PRUNE && c0 == 0 && tid == 0) s_misc[4] = p.residual ? (int)0x80000000u : 0;
           uint64_t total;
           uint64_t ex = block_exclusive_scan_u64<NW>(mine, s_warp, &total);
           if (PRUNE && un_mine) atomicAdd((unsigned*)&s_misc[4], un_mine);
@@ -904,7 +910,7 @@ template <int B, int KS, int NW>
 cudaError_t launch_main(const QP& p, int sms, cudaStream_t st) {
   if constexpr (B * KS <= 24 && B <= NW) {
     if constexpr (B == 1 && NW == 4) {  // the auto shape of indexes without head features
-      if (p.prune_suf)  // pruned queries (a6)
+      if (p.prune_suf || p.residual)  // pruned queries (a6), residual completion (f1)
         return p.vals ? launch_main4<B, KS, true, NW, false, true>(p, sms, st)
                       : launch_main4<B, KS, false, NW, false, true>(p, sms, st);
       if (!p.head_smem)

@@ -35,7 +35,9 @@ struct IndexLayout {
          fwd_ptr_at = 0, fwd_idx_at = 0, fwd_val_at = 0, fmax_at = 0, total = 0;
 };
 // prune: also reserve S's forward rows and (INT8 S) the per-feature maximum weight (pruned queries, a6)
-bool index_layout(const knnjoin_csr* S, int32_t d, int32_t tile, bool prune, IndexLayout* L);
+// F: the CSR whose rows are kept as forward rows (S itself, or options.forward)
+bool index_layout(const knnjoin_csr* S, int32_t d, int32_t tile, bool prune, IndexLayout* L,
+                  const knnjoin_csr* F = nullptr);
 constexpr float kDefaultPruneAlpha = 0.25f;
 int32_t resolve_tile(const knnjoin_options* opt);
 

@@ -43,7 +43,8 @@ int32_t resolve_tile(const knnjoin_options* opt) {
   return t;
 }
 
-bool index_layout(const knnjoin_csr* S, int32_t d, int32_t tile, bool prune, IndexLayout* L) {
+bool index_layout(const knnjoin_csr* S, int32_t d, int32_t tile, bool prune, IndexLayout* L, const knnjoin_csr* F) {
+  if (!F) F = S;
   if (!S || d <= 0 || tile <= 0 || S->n_rows < 0 || S->nnz < 0) return false;
   L->n_tiles = (S->n_rows + tile - 1) / tile;
   L->n_off = (int64_t)d * (L->n_tiles + 1) + 1;
@@ -70,9 +71,9 @@ bool index_layout(const knnjoin_csr* S, int32_t d, int32_t tile, bool prune, Ind
     L->fwd_ptr_at = at;
     at = align_up(at + sizeof(int64_t) * (size_t)(S->n_rows + 1), 256);
     L->fwd_idx_at = at;
-    at = align_up(at + sizeof(int32_t) * (size_t)S->nnz, 256);
+    at = align_up(at + sizeof(int32_t) * (size_t)F->nnz, 256);
     L->fwd_val_at = at;
-    if (S->dtype == KNNJOIN_INT8) at = align_up(at + (size_t)S->nnz, 256);
+    if (S->dtype == KNNJOIN_INT8) at = align_up(at + (size_t)F->nnz, 256);
     L->fmax_at = at;
     if (S->dtype == KNNJOIN_INT8) at = align_up(at + sizeof(uint32_t) * (size_t)d, 256);
   }
@@ -136,6 +137,14 @@ bool check_build_args(const knnjoin_csr* S, int32_t d, const knnjoin_options* op
     return false;
   }
   if (opt && opt->head_max > kMaxHead) { set_error("head_max must be <= %d", kMaxHead); return false; }
+  if (opt && opt->forward) {
+    const knnjoin_csr* F = opt->forward;
+    if (!opt->prune) { set_error("options.forward needs prune = 1"); return false; }
+    if (F->n_rows != S->n_rows || F->dtype != S->dtype || F->nnz < 0) {
+      set_error("options.forward must have S's row count and dtype");
+      return false;
+    }
+  }
   if ((int64_t)d * ((S->n_rows + *tile - 1) / *tile + 1) + 1 >= ((int64_t)1 << 31)) {
     set_error("d * (n_tiles+1) too large for 32-bit slice keys; shard S or raise the tile width");
     return false;
@@ -446,7 +455,7 @@ KJ_API size_t knnjoin_index_bytes(const knnjoin_csr* S, int32_t d, const knnjoin
   int32_t tile;
   if (!check_build_args(S, d, opt, &tile)) return 0;
   IndexLayout L;
-  if (!index_layout(S, d, tile, opt && opt->prune, &L)) { set_error("bad index layout arguments"); return 0; }
+  if (!index_layout(S, d, tile, opt && opt->prune, &L, opt ? opt->forward : nullptr)) { set_error("bad index layout arguments"); return 0; }
   return L.total;
 }
 
@@ -455,7 +464,7 @@ KJ_API size_t knnjoin_build_workspace_bytes(const knnjoin_csr* S, int32_t d, con
   if (!check_build_args(S, d, opt, &tile)) return 0;
   IndexLayout L;
   BuildWs W;
-  if (!index_layout(S, d, tile, opt && opt->prune, &L) || !build_ws_layout(S, d, L, &W)) { set_error("workspace sizing failed"); return 0; }
+  if (!index_layout(S, d, tile, opt && opt->prune, &L, opt ? opt->forward : nullptr) || !build_ws_layout(S, d, L, &W)) { set_error("workspace sizing failed"); return 0; }
   return W.total;
 }
 
@@ -476,7 +485,7 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   if (S->dtype == KNNJOIN_INT8 && S->nnz > 0 && !S->values) { set_error("INT8 S needs values"); return KNNJOIN_ERR_ARG; }
   IndexLayout L;
   BuildWs W;
-  if (!index_layout(S, d, tile, opt && opt->prune, &L) || !build_ws_layout(S, d, L, &W)) { set_error("layout failed"); return KNNJOIN_ERR_ARG; }
+  if (!index_layout(S, d, tile, opt && opt->prune, &L, opt ? opt->forward : nullptr) || !build_ws_layout(S, d, L, &W)) { set_error("layout failed"); return KNNJOIN_ERR_ARG; }
   if (!storage || storage_bytes < L.total) { set_error("index storage %zu < %zu bytes", storage_bytes, L.total); return KNNJOIN_ERR_WORKSPACE; }
   if (!workspace || workspace_bytes < W.total) { set_error("build workspace %zu < %zu bytes", workspace_bytes, W.total); return KNNJOIN_ERR_WORKSPACE; }
   if (((uintptr_t)storage & 255) || ((uintptr_t)workspace & 255)) { set_error("storage and workspace must be 256-byte aligned"); return KNNJOIN_ERR_ARG; }
@@ -556,21 +565,26 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   int32_t* fwd_idx = nullptr;
   uint8_t* fwd_val = nullptr;
   uint32_t* fmax = nullptr;
-  if (prune) {  // forward rows for the exact completions of pruned queries (a6)
+  if (prune) {  // forward rows for the exact completions of pruned queries (a6) / residual rows s' (f1)
+    const knnjoin_csr* F = opt->forward ? opt->forward : S;
+    if (F->n_rows > 0 && (!F->indptr || (F->nnz > 0 && (!F->indices || (S->dtype == KNNJOIN_INT8 && !F->values))))) {
+      set_error("forward CSR pointers are NULL");
+      return KNNJOIN_ERR_ARG;
+    }
     fwd_ptr = (int64_t*)(sb + L.fwd_ptr_at);
     fwd_idx = (int32_t*)(sb + L.fwd_idx_at);
-    if (S->n_rows > 0 &&
-        (e = cudaMemcpyAsync(fwd_ptr, S->indptr, 8 * (size_t)(S->n_rows + 1), cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+    if (F->n_rows > 0 &&
+        (e = cudaMemcpyAsync(fwd_ptr, F->indptr, 8 * (size_t)(F->n_rows + 1), cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
       return cuda_fail(e, "copy forward indptr");
-    if (S->n_rows == 0 && (e = cudaMemsetAsync(fwd_ptr, 0, 8, st)) != cudaSuccess) return cuda_fail(e, "memset indptr");
-    if (S->nnz > 0 &&
-        (e = cudaMemcpyAsync(fwd_idx, S->indices, 4 * (size_t)S->nnz, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+    if (F->n_rows == 0 && (e = cudaMemsetAsync(fwd_ptr, 0, 8, st)) != cudaSuccess) return cuda_fail(e, "memset indptr");
+    if (F->nnz > 0 &&
+        (e = cudaMemcpyAsync(fwd_idx, F->indices, 4 * (size_t)F->nnz, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
       return cuda_fail(e, "copy forward indices");
     if (S->dtype == KNNJOIN_INT8) {
       fwd_val = (uint8_t*)(sb + L.fwd_val_at);
       fmax = (uint32_t*)(sb + L.fmax_at);
-      if (S->nnz > 0 &&
-          (e = cudaMemcpyAsync(fwd_val, S->values, (size_t)S->nnz, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+      if (F->nnz > 0 &&
+          (e = cudaMemcpyAsync(fwd_val, F->values, (size_t)F->nnz, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
         return cuda_fail(e, "copy forward values");
       if ((e = cudaMemsetAsync(fmax, 0, 4 * (size_t)d, st)) != cudaSuccess) return cuda_fail(e, "memset fmax");
       if (S->nnz > 0) {

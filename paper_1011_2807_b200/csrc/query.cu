@@ -517,6 +517,12 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
     return KNNJOIN_ERR_ARG;
   }
   if (idx->prune) alpha = (qopt && qopt->prune_alpha != 0.0f) ? (qopt->prune_alpha > 0.0f ? qopt->prune_alpha : 0.0f) : idx->alpha;
+  const bool residual = qopt && qopt->residual;
+  if (residual) {
+    if (!idx->prune) { set_error("residual queries need an index built with prune = 1 (forward rows = s')"); return KNNJOIN_ERR_ARG; }
+    if (qopt->prune_alpha > 0.0f) { set_error("residual (f1) and prune_alpha > 0 (a6) are exclusive"); return KNNJOIN_ERR_ARG; }
+    alpha = 0.0f;
+  }
   const bool auto_shape = !qopt || (qopt->batch_rows == 0 && qopt->cta_warps == 0);
   if (auto_shape && idx->n_head_host < 0) {
     // first auto-shaped query on this index: read its head count once (4-byte copy; synchronises `stream`)
@@ -540,11 +546,11 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
               (long long)idx->n_tiles);
     return KNNJOIN_ERR_ARG;
   }
-  if (alpha > 0.0f && (size_t)((idx->d + 31) / 32) * 4 + smem_bytes(1, idx->tile, k, 4, false) > 200 * 1024) {
+  if ((alpha > 0.0f || residual) && (size_t)((idx->d + 31) / 32) * 4 + smem_bytes(1, idx->tile, k, 4, false) > 200 * 1024) {
     set_error("pruned queries keep a d-bit map in shared memory: d = %d too large", idx->d);
     return KNNJOIN_ERR_UNSUPPORTED;
   }
-  if (alpha > 0.0f && !(sh.B == 1 && sh.NW == 4)) {
+  if ((alpha > 0.0f || residual) && !(sh.B == 1 && sh.NW == 4)) {
     set_error("pruned queries run one-row 4-warp CTAs (batch_rows 1, cta_warps 4); got %d / %d", sh.B, sh.NW);
     return KNNJOIN_ERR_UNSUPPORTED;
   }
@@ -691,6 +697,7 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
   p.fwd_val = idx->fwd_val;
   p.fmax = idx->fmax;
   p.prune_words = (idx->d + 31) / 32;
+  p.residual = residual ? 1 : 0;
   p.state_keys = state_keys;
   p.pass_done = pass_done;
   p.counters = (unsigned long long*)(qopt ? qopt->counters : nullptr);
