@@ -202,9 +202,14 @@ def cpu_baseline(cfg, R, S, budget_s=15.0):
     rows = rng.choice(R.n_rows, size=n_rows, replace=False)
     t = run_oracle_sample(cfg, R, S, rows, cores)
     pairs = n_rows * S.n_rows
+    # the same oracle on ONE core (1 core, then all cores), on a few rows of that sample
+    n1 = int(max(1, min(n_rows, budget_s / 5.0 / max(per_row, 1e-9))))
+    t1 = run_oracle_sample(cfg, R, S, rows[:n1], 1)
     return {"value": pairs / t, "unit": "pairs/s", "cores": cores, "kind": "oracle",
             "sample": f"{n_rows} random rows of R x all {S.n_rows} rows of S ({pairs:.3e} pairs, {t:.1f} s), "
-                      f"single-threaded C oracle per thread, rows split over {cores} host threads"}
+                      f"single-threaded C oracle per thread, rows split over {cores} host threads",
+            "value_1core": n1 * S.n_rows / t1,
+            "sample_1core": f"{n1} of those rows on one thread ({n1 * S.n_rows:.3e} pairs, {t1:.1f} s)"}
 
 
 def bench_reference(args):
