@@ -336,6 +336,15 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
     phase_mark(5);
 
     const int64_t t_stop = nruns > 0 ? t_end : t_begin;
+    // batches whose runs fit one staging chunk: the runs' features are loaded once per item instead of once
+    // per tile (one dependent L2 round trip less in every stage)
+    const bool one_chunk = nruns <= kCap;
+    uint32_t fm_c[IPT];
+#pragma unroll
+    for (int it = 0; it < IPT; ++it) {
+      const int li = tid + it * NT_;
+      fm_c[it] = (one_chunk && li < kCap && li < nruns) ? __ldg(p.runs_f + run_base + li) : 0u;
+    }
     for (int64_t t = t_begin; t < t_stop; ++t) {
       // a6: the non-essential budget of this tile, from the row's k-th key so far (every thread reads the same
       // value: s_theta is only written during scans, which are fenced by __syncthreads)
@@ -361,7 +370,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
             const int i = c0 + li;
             fm[it] = 0; u0[it] = 0; U[it] = 0;
             if (li < kCap && i < nruns) {
-              fm[it] = p.runs_f[(size_t)(run_base + i)];
+              fm[it] = one_chunk ? fm_c[it] : p.runs_f[(size_t)(run_base + i)];
               const uint32_t* o = p.off + (size_t)(fm[it] & 0xFFFFFFu) * (size_t)(p.NT + 1) + (size_t)t;
               u0[it] = o[0];
               U[it] = o[1] - u0[it];
