@@ -102,3 +102,31 @@ def test_ctypes_structs_match_the_c_header(tmp_path):
         assert int(got[cname]) == ctypes.sizeof(cls), cname
         for f, _ in cls._fields_:
             assert int(got[f"{cname}.{f}"]) == getattr(cls, f).offset, f"{cname}.{f}"
+
+
+def test_iiib_host_sizes_and_errors():
+    """f1 building blocks: host-only size queries and argument errors (no device access)."""
+    import paper_1011_2807_b200._binding as b
+    L = b._lib
+    R = b._CSR(1000, 40_000, 0, 0, 0, b.FP32)
+    S = b._CSR(10_000, 400_000, 0, 0, 0, b.BINARY)
+    # (the profile / split sizes include CUB scratch, whose size query needs a device: GPU tests cover them)
+    assert L.knnjoin_iiib_profile_bytes(ctypes.byref(R), 0) == 0 and "d <= 0" in b.knnjoin_last_error()
+    assert L.knnjoin_iiib_threshold_workspace_bytes(ctypes.byref(R)) >= 16 * 1000
+    # NULL profile / threshold -> ERR_ARG before any device work
+    st = L.knnjoin_iiib_split(ctypes.byref(S), 10_000, None, None, 1, None, None, None, None, None, None, None, 0, None)
+    assert st == 1 and "iiib_split" in b.knnjoin_last_error()
+    # forward rows need prune = 1 and S's row count
+    F = b._CSR(10_000, 100, 0, 0, 0, b.BINARY)
+    opt = b._Options(8192, 0, 0.0, 0.0, 0, ctypes.addressof(F))
+    assert L.knnjoin_index_bytes(ctypes.byref(S), 10_000, ctypes.byref(opt)) == 0
+    assert "forward" in b.knnjoin_last_error()
+    F2 = b._CSR(9_999, 100, 0, 0, 0, b.BINARY)
+    opt = b._Options(8192, 1, 0.0, 0.0, 0, ctypes.addressof(F2))
+    assert L.knnjoin_index_bytes(ctypes.byref(S), 10_000, ctypes.byref(opt)) == 0
+    # with a matching forward CSR the storage holds ITS rows (100 entries), not S's
+    opt = b._Options(8192, 1, 0.0, 0.0, 0, ctypes.addressof(F))
+    a = L.knnjoin_index_bytes(ctypes.byref(S), 10_000, ctypes.byref(opt))
+    base = L.knnjoin_index_bytes(ctypes.byref(S), 10_000, ctypes.byref(b._Options(8192, 0, 0.0, 0.0, 0, None)))
+    al = lambda x: (x + 255) // 256 * 256
+    assert a == base + al(8 * 10_001) + al(4 * 100)
