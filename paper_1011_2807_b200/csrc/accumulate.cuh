@@ -495,7 +495,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
                 off4[j] = ((wd[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu) * 4u;
-                w8[j] = wint8 ? (((j < 4 ? S.w.x : S.w.y) >> (8 * (j & 3))) & 0xFFu) : 1u;
+                // byte j & 3 zero-extended in one PRMT (selector nibbles 4 = a zero byte of the second operand)
+                w8[j] = wint8 ? __byte_perm(j < 4 ? S.w.x : S.w.y, 0u, 0x4440u | (uint32_t)(j & 3)) : 1u;
               }
 #pragma unroll
               for (int b = 0; b < B; ++b) {
