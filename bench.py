@@ -159,8 +159,19 @@ def smem_roofline(id_visits, pairs, kernel_ms, clocks, sms):
     peak = sms * 128 * mhz * 1e6 / 1e12  # TB/s
     alg = 4 * id_visits + 8 * pairs
     ach = alg / (kernel_ms * 1e-3) / 1e12
+    # op-rate form: shared atomics and the dense scan are limited by wavefronts, not bytes; the measured chip-wide
+    # rates of tools/microbench.cu on a B200 (profiles/r1k_microbench.txt, 1965 MHz): red.shared to random banks
+    # 2.63e12 lane-ops/s (5.83e12 conflict-free), scan + zero-fill 4.63e12 pairs/s
+    atom_rand, atom_cf, scan_rate = 2.63e12, 5.83e12, 4.63e12
+    t_rand = (id_visits / atom_rand + pairs / scan_rate) * 1e3
+    t_cf = (id_visits / atom_cf + pairs / scan_rate) * 1e3
     return {"bound": "smem", "achieved": ach, "peak": peak, "unit": "TB/s", "frac": ach / peak,
-            "algorithmic_bytes": alg, "peak_source": f"derived: {sms} SMs x 128 B/clk x {mhz:.0f} MHz (sampled)"}
+            "algorithmic_bytes": alg, "peak_source": f"derived: {sms} SMs x 128 B/clk x {mhz:.0f} MHz (sampled)",
+            "op_bound_ms": {"random_banks": t_rand, "conflict_free": t_cf},
+            "op_frac": {"random_banks": t_rand / kernel_ms, "conflict_free": t_cf / kernel_ms},
+            "op_note": "id-list visits / measured shared-atomic rate + pairs / measured scan rate "
+                       "(tools/microbench.cu, profiles/r1k_microbench.txt): the time the kernel's shared-memory "
+                       "work alone needs; op_frac = that / kernel time"}
 
 
 def head_visits(R, S, d, head_min_df, head_max=32):
