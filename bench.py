@@ -562,6 +562,8 @@ def bench_ours(args):
         "gpu_launches": (launches_per_step * args.steps) if launches_per_step is not None else None,
         "breakdown": {"kernel_ms": kern_avg_max, "step_ms": ms_per_step,
                       "build_index_ms": sum(build_ms) / len(build_ms),
+                      # a2 reported separately: postings of S indexed per second
+                      "build_postings_per_s": int(S.nnz) / (sum(build_ms) / len(build_ms) * 1e-3),
                       "query_prep_ms": ms_per_step - kern_avg_max - sum(build_ms) / len(build_ms),
                       "other_ms": ms_per_step - kern_avg_max, "launches_per_step": launches_per_step,
                       "kernel_phase_share": phase_share, "counters": counters},
