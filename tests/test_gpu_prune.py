@@ -160,3 +160,20 @@ def test_full_size_pruned_equals_unpruned(name, alphas):
     o_ids, o_sc = oracle.knn(R, S, c.k, rows=rows, threads=max(1, min(8, len(os.sched_getaffinity(0)))))
     assert_parity(R.take_rows(rows), S, i1.cpu().numpy()[rows].astype(np.int64),
                   s1.cpu().numpy()[rows].astype(np.float64), o_ids, o_sc, rows=None)
+
+
+def test_pruned_edge_cases():
+    """Empty rows, R features >= d (ignored), k > #positives, empty S, one-posting slices."""
+    d = 64
+    R = csr_from_rows([[0, 1, 2], [], [63], [5, 6], [(0)]], d, "binary")
+    S = csr_from_rows([[0], [], [1, 2, 3], [63], [7], [0, 1, 2, 5, 6]] * 700, d, "binary")
+    for k in (1, 4, 7):
+        _pruned_equals_unpruned(R, S, k, 2048, (0.25, 1.0))
+    Rw = csr_from_rows([[0, 70, 80], [1, 2, 90]], 128, "binary")
+    Sw = csr_from_rows([[0], [0, 1], [1, 2]] * 1000, 128, "binary")
+    _pruned_equals_unpruned(Rw, Sw, 3, 2048, (0.5, 1.0), d=64, oracle_check=False)
+    import paper_1011_2807_b200 as kj
+    Sempty = csr_from_rows([], d, "binary")
+    idx = kj.knnjoin_build_index(kj.DeviceCSR.from_host(Sempty), d, prune=1, alpha=1.0)
+    ids, sc, _ = kj.knnjoin_query(idx, kj.DeviceCSR.from_host(R), 3)
+    assert (ids == -1).all() and (sc == 0).all()
