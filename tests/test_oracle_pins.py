@@ -10,7 +10,7 @@ import pytest
 
 import oracle
 from oracle import paper_algs as pa
-from tests.util import csr_from_rows, random_csr, scipy_topk
+from tests.util import csr_from_rows, random_csr, scipy_topk, stable_seed
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
@@ -83,7 +83,7 @@ def test_hand_example_ties_and_padding():
 @pytest.mark.parametrize("k", [1, 3, 7, 40])
 def test_knn_matches_scipy_spgemm_and_lexsort(dtype_r, dtype_s, k):
     """The oracle top-k == textbook SpGEMM R @ S.T followed by lexsort (score desc, id asc)."""
-    rng = np.random.default_rng(hash((dtype_r, dtype_s, k)) % 2**32)
+    rng = np.random.default_rng(stable_seed(dtype_r, dtype_s, k))
     d = 40
     R = random_csr(rng, 25, d, 0, 12, dtype_r, vmax=3)
     S = random_csr(rng, 60, d, 0, 12, dtype_s, vmax=3)

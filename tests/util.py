@@ -62,3 +62,9 @@ def scipy_topk(R, S, k):
         ids[i, :len(order)] = pos[order]
         sc[i, :len(order)] = row[pos[order]]
     return ids, sc, M
+
+
+def stable_seed(*parts) -> int:
+    """A per-case seed that is the same in every process (Python's hash() of strings is salted per process)."""
+    import zlib
+    return zlib.crc32(repr(parts).encode())
