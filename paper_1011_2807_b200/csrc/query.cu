@@ -1,4 +1,5 @@
-// query.cu -- K2 (query prep) and K3 (score accumulation fused with per-tile top-k) of the KNN join.
+// query.cu -- K2 (query prep) and the host side of K3 (score accumulation fused with per-tile top-k; the kernel
+// itself is in accumulate.cuh) of the KNN join.
 //
 // What is computed: for every r in R, Find_Matches_IIB (Alg. 3 lines 9-17):
 //   A[s] += r[d] * s[d] for every posting (s, s[d]) of I_d, for every feature (d, r[d]) of r  (a4)
@@ -7,22 +8,16 @@
 //
 // GPU mapping:
 //  * k_row_scale  (a3) per-row fixed-point scale sigma_r = 2^30 / (sum_d r_d * smax) for FP32 R, 1 otherwise.
-//  * k_build_runs (a3) one warp per batch of B rows: B-way merge of the rows' ascending feature lists
-//    into "runs" (feature f, mask of batch rows that contain f, q_b = r_b[f] quantised).  A run's
-//    posting slice is loaded once and applied to every row in its mask (cross-row reuse).
-//  * k_accumulate_topk (a4 + a5 + a7), persistent, one CTA (16 warps) per SM:
-//      for each batch (B rows) taken from a global counter:
-//        for each S tile t (ascending, so ids arrive in ascending order):
-//          stage: every thread reads the (f, t) slice bounds of one run; a block scan compacts
-//                 non-empty runs and gives each its position P in the tile's flattened unit stream.
-//          accumulate: each warp owns a contiguous range of 32-unit windows of that stream; lane l
-//                 takes unit p0+l, finds its run by a 5-step shuffle search, loads 16 B (8 local ids,
-//                 + 8 INT8 weights) with ld.global.nc, and issues atomicAdd(acc[b][id], q_b*w) for each
-//                 row b of the run.  Integer atomics make the sum order-independent (bit-reproducible).
-//          scan:  warp w owns columns [w*T/16, (w+1)*T/16) of every row: 128-bit reads, zero-fill, and
-//                 candidates with key > theta go into the warp's register top-k list; theta_row (shared,
-//                 atomicMax of every warp's k-th key) tightens every warp's filter.
-//        merge the 16 per-warp lists of each row, finalize (ids, scores, keys).
+//  * k_row_work + CUB sort (a3) rows ordered by their work w_r = sum_{d in r} |I_d|, heaviest batches first.
+//  * k_build_runs (a3) one CTA per batch of B rows: block radix sort of the rows' (feature, row) entries into
+//    "runs" (feature f, mask of batch rows that contain f, q_b = r_b[f] quantised).  A run's posting slice
+//    is loaded once and applied to every row in its mask (cross-row reuse).
+//  * k_prune_prep (a6, pruned queries) per-row suffix bounds of the c-descending feature order.
+//  * knnjoin_query: workspace layout, the CTA shape (pick_shape: 8-warp CTAs with B = 2 rows for indexes with
+//    head features, 4-warp one-row CTAs otherwise), pass slabs sized for L2 or the small-R tile-group split,
+//    and the launch of k_accumulate_topk (accumulate.cuh: per tile, stage the runs' slice bounds, accumulate
+//    with shared-memory atomics over contiguous per-warp window ranges, scan + top-k per warp column strip;
+//    per batch, merge the warps' lists by rank and write ids / scores / keys).
 #include <cub/cub.cuh>
 
 #include "accumulate.cuh"
