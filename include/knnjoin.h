@@ -94,16 +94,16 @@ typedef struct {
  *  batch_rows: R rows per CTA batch (0 = auto).
  *  cta_warps:  warps per CTA of the accumulation kernel, 4, 8 or 16.  Auto (batch_rows and cta_warps both
  *              0): an index without head features gets 4-warp one-row CTAs, six per SM; one with head features
- *              gets 8-warp CTAs, three (or two) per SM, with the largest batch whose score arrays fit.  To
- *              choose, the first auto-shaped query on an index reads the index's head count (a 4-byte
- *              device-to-host copy that synchronises `stream` once per index).
+ *              gets 8-warp CTAs, three (or two) per SM, with the largest batch whose score arrays fit.  The head
+ *              count is known on the device only, so for a BINARY-S index with head features enabled both
+ *              candidate shapes are launched and each returns at entry unless it matches the count: the call
+ *              never synchronises and is always capturable in a CUDA graph.
  *  tiles_per_pass: S tiles swept by all batches before any batch moves on (0 = auto: about a third of the
  *              L2 cache worth of index per pass; the whole index when it fits).  Top-k state is carried
  *              between passes in the workspace; results do not depend on it.  Auto also splits the tiles
  *              into independent groups when R has fewer batches than two waves of resident CTAs (small R,
  *              serving): each group's lists are merged by rank after the kernel (K4), same result.
- *  Graph capture: after the first query on an index (which reads the index statistics, see cta_warps),
- *              knnjoin_query issues only stream-ordered work and may be captured into a CUDA graph.
+ *  Graph capture: knnjoin_query issues only stream-ordered work and may be captured into a CUDA graph.
  *  counters:   NULL, or a device int64_t[4] that the query ADDS into: [0] postings visited (Eq. 4 second
  *              term; head postings are counted whether or not their completion is skipped),
  *              [1] candidate inserts into the top-k lists, [2] head postings whose exact addition was skipped
@@ -140,7 +140,27 @@ typedef struct {
  *              parts s'' of its S rows and its forward rows are the residual parts s' (knnjoin_iiib_split):
  *              every s with a non-zero partial score is completed with dot(r, s') (line 21) before the
  *              candidate test.  Needs an index built with prune = 1; not combinable with prune_alpha > 0.
- *              counters [3] counts the completions. */
+ *              counters [3] counts the completions.
+ *  precision:  score arithmetic.  0 (auto, default): FP32-R queries accumulate in 32-bit per-row
+ *              fixed point; every row's final list is then certified -- with E_r = smax * sum_d |q_d - r_d sigma_r|
+ *              the bound on any pair's absolute error and y_min the smallest positive score of the list, the list
+ *              meets the tolerance rule of DESIGN.md reading c15 when E_r (2 + tol) <= (tol - 2^-23) y_min -- and
+ *              the rows that fail are recomputed at 64-bit fixed point (wide.cu), which holds the rule at any
+ *              dynamic range of practical inputs (weights spanning many decades).  Auto skips the
+ *              recomputation in a partial query (tile range, resume_keys or theta_in): the caller certifies the
+ *              complete lists with knnjoin_certify.  1: 32-bit only (with `uncertified`, the failing rows are
+ *              reported, not recomputed).  2: 64-bit for every row.  Integer R with integer S is exact at 32 bits
+ *              (precision is ignored); FP32 S always runs at 64 bits (1 -> KNNJOIN_ERR_UNSUPPORTED).
+ *              KEY ENCODING: 32-bit results key the fixed-point score (score field = the row's fixed-point sum,
+ *              decoded with the row's scale); 64-bit results key the fp32 score itself (score field = fp32 bits of
+ *              the score; candidates within fp32 rounding tie and go to the lower id).  Rows recomputed by auto
+ *              mode therefore carry fp32-keyed out_keys; they are the rows listed in `uncertified`.
+ *  row_list / row_count: 64-bit queries only: NULL, or device int32 rows of R to process (input row numbers) and
+ *              a device int32 count; other rows' outputs are left untouched.
+ *  uncertified: NULL, or device int32[1 + R.n_rows]: [0] = number of rows whose 32-bit list fails the
+ *              certification (auto: the rows recomputed at 64 bits), followed by those rows in no particular order.
+ *              Written by every query (count 0 when nothing was certified: integer inputs, 64-bit queries).
+ *  tolerance:  relative tolerance of the certification (0 = 1e-5, BASELINE.json north_star). */
 typedef struct {
   int32_t batch_rows;
   int64_t* counters;
@@ -156,6 +176,11 @@ typedef struct {
   const uint64_t* theta_in;
   float prune_alpha;
   int32_t residual;
+  int32_t precision;
+  const int32_t* row_list;
+  const int32_t* row_count;
+  int32_t* uncertified;
+  float tolerance;
 } knnjoin_query_options;
 
 typedef struct knnjoin_index knnjoin_index; /* opaque HOST handle; borrows the caller's index storage */
@@ -185,7 +210,7 @@ size_t knnjoin_index_bytes(const knnjoin_csr* S, int32_t d, const knnjoin_option
 /* Bytes of device scratch knnjoin_build_index needs (sort buffers and scan temporaries). */
 size_t knnjoin_build_workspace_bytes(const knnjoin_csr* S, int32_t d, const knnjoin_options* opt);
 
-/* Build the tiled inverted index of S into `index_storage` (>= knnjoin_index_bytes bytes, 256-byte
+/* Build the tiled inverted index of S (BINARY, INT8 or FP32 weights) into `index_storage` (>= knnjoin_index_bytes bytes, 256-byte
  * aligned) using `workspace` (>= knnjoin_build_workspace_bytes bytes).  Layout:
  * for tile t (S ids [t*tile, (t+1)*tile)) and feature f, the postings of I_f restricted to the tile are a
  * contiguous, 16-byte aligned slice of local ids (+ uint8 values for INT8 S), padded with dummy ids
@@ -194,8 +219,8 @@ size_t knnjoin_build_workspace_bytes(const knnjoin_csr* S, int32_t d, const knnj
  * are stored as one 32-bit word per S row instead of id lists.
  * s_id_base: global id of S row 0 (ids returned by queries are s_id_base + local row).
  * S may be freed after the call's work completes on `stream`; the storage must outlive every query.
- * S dtype must be BINARY or INT8 (FP32 S -> KNNJOIN_ERR_UNSUPPORTED).  *out receives a host handle
- * to release with knnjoin_free_index. */
+ * FP32 S stores its weights as fp32 (6 bytes per posting) and is queried at 64-bit fixed point (precision);
+ * prune = 1 needs BINARY or INT8 S.  *out receives a host handle to release with knnjoin_free_index. */
 knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64_t s_id_base, const knnjoin_options* opt,
                                    void* index_storage, size_t storage_bytes, void* workspace, size_t workspace_bytes,
                                    void* stream, knnjoin_index** out);
@@ -211,11 +236,11 @@ size_t knnjoin_query_workspace_bytes(const knnjoin_index* idx, const knnjoin_csr
 
 /* For every row r of R (1 <= k <= 256) write, in rank order (score desc, id asc):
  *   out_ids[r*k + i]    int32  global S id, or -1 for padding;
- *   out_scores[r*k + i] float  dot(r, s) (exact for BINARY/INT8 R; for FP32 R the per-row fixed-point
- *                              sum / scale, relative error ~1e-8);
+ *   out_scores[r*k + i] float  dot(r, s): exact for BINARY/INT8 R and S; otherwise the fixed-point sum / scale,
+ *                              within the certified tolerance (see precision);
  *   out_keys[r*k + i]   uint64 (optional, may be NULL) the packed ordering key
  *                              (score_u32 << 32) | (0xFFFFFFFF - global_id), 0 for padding, as consumed by
- *                              knnjoin_merge (S-sharded multi-GPU).
+ *                              knnjoin_merge (S-sharded multi-GPU); score_u32 per `precision`'s key encoding.
  * out_ids / out_scores may be NULL when out_keys is given.  R dtype: BINARY, INT8 or FP32.
  * Integer (BINARY/INT8 x BINARY/INT8) scores must fit in 32 bits: d * 127 * 127 < 2^32, else UNSUPPORTED.
  * Empty R: nothing is written.  Empty S: every row is padding. */
@@ -227,6 +252,16 @@ knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr* R, int
 
 size_t knnjoin_merge_workspace_bytes(const knnjoin_csr* R);
 
+/* Merge options (NULL = defaults).  float_keys: 1 = the keys carry fp32 scores (64-bit queries; implied for FP32
+ * S), 0 = 32-bit fixed-point scores decoded with R's per-row scale.  row_list / row_count: NULL, or device int32
+ * rows and a device count: only the listed rows are merged and written (the 64-bit re-run of uncertified rows in
+ * a sharded join); their lists sit at their own row positions of the [P][n_rows][k] slabs. */
+typedef struct {
+  int32_t float_keys;
+  const int32_t* row_list;
+  const int32_t* row_count;
+} knnjoin_merge_options;
+
 /* keys: uint64[P][n_rows][k] (each [n_rows][k] slab is one shard's out_keys, e.g. gathered by an NCCL
  * all-gather): every row of every slab sorted descending with its 0 padding last, and the P slabs from
  * disjoint S id ranges (distinct keys), as knnjoin_query writes them.  Each merged key is placed by rank
@@ -235,8 +270,18 @@ size_t knnjoin_merge_workspace_bytes(const knnjoin_csr* R);
  * per-row score scale, exactly as knnjoin_query computed it.
  * The merge is exact: keys encode (score, lower-id-wins) as one unsigned integer. */
 knnjoin_status knnjoin_merge(const uint64_t* keys, int32_t P, const knnjoin_csr* R, int32_t d,
-                             knnjoin_dtype s_dtype, int32_t k, uint64_t* out_keys, int32_t* out_ids, float* out_scores, void* workspace,
-                             size_t workspace_bytes, void* stream);
+                             knnjoin_dtype s_dtype, int32_t k, const knnjoin_merge_options* mopt, uint64_t* out_keys,
+                             int32_t* out_ids, float* out_scores, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- certification of 32-bit fixed-point lists -------------------------------------------
+ * keys: uint64[n_rows][k], complete 32-bit lists of FP32 R (e.g. knnjoin_merge's output of a sharded join, or
+ * the last of a chain of resumed queries), s_dtype BINARY or INT8 (the scale knnjoin_query used).  Writes to
+ * out_list (device int32[1 + n_rows]) the count and the rows whose lists fail the tolerance rule (see
+ * knnjoin_query_options.precision); integer R: count 0.  The caller then recomputes those rows with a 64-bit
+ * query (precision 2, row_list = out_list + 1, row_count = out_list) and merges with float_keys = 1. */
+size_t knnjoin_certify_workspace_bytes(const knnjoin_csr* R);
+knnjoin_status knnjoin_certify(const uint64_t* keys, const knnjoin_csr* R, int32_t d, knnjoin_dtype s_dtype, int32_t k,
+                               float tolerance, int32_t* out_list, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- f1: IIIB-literal (Alg. 4) building blocks --------------------------------------
  * The paper's improved algorithm per (R block, S block): dimensions reordered by their non-zero count in the

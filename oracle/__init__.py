@@ -7,6 +7,8 @@ no code with it.
 * ``oracle.c``       -- the plain single-threaded brute-force definition (§3 Eq. 1 with the
                         merge dot of Alg. 2 lines 8-23), ties to the lower S id, zero
                         scores excluded, padded with (-1, 0).
+* ``iib.c``          -- the paper's IIB (Alg. 3) in plain single-threaded C: the "paper's method
+                        on the host" leg of bench.py's cpu_baseline (not an oracle; pinned against oracle_knn).
 * ``paper_algs.py``  -- the paper's Alg. 1-4 (block nested loops, BF, IIB, IIIB) written out step by step
                         in pure Python, with the Eq. 2-4 cost counters, for tiny cross-check instances.
 
@@ -38,11 +40,13 @@ class _CSR(ctypes.Structure):
                 ("values", ctypes.c_void_p), ("dtype", ctypes.c_int32)]
 
 
+_SOURCES = ("oracle.c", "iib.c")
+
+
 def build() -> str:
-    """Compile oracle.c (plain C, -O2, no OpenMP: the oracle is single-threaded)."""
-    src = os.path.join(_HERE, "oracle.c")
+    """Compile oracle.c + iib.c (plain C, -O2, no OpenMP: both are single-threaded)."""
     tmp = _SO + f".tmp{os.getpid()}"
-    subprocess.check_call(["gcc", "-O2", "-shared", "-fPIC", "-o", tmp, src])
+    subprocess.check_call(["gcc", "-O2", "-shared", "-fPIC", "-o", tmp] + [os.path.join(_HERE, f) for f in _SOURCES])
     os.replace(tmp, _SO)
     return _SO
 
@@ -51,8 +55,8 @@ def lib():
     global _lib
     with _lock:
         if _lib is None:
-            src = os.path.join(_HERE, "oracle.c")
-            if not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
+            newest = max(os.path.getmtime(os.path.join(_HERE, f)) for f in _SOURCES)
+            if not os.path.exists(_SO) or os.path.getmtime(_SO) < newest:
                 build()
             L = ctypes.CDLL(_SO)
             P = ctypes.POINTER(_CSR)
@@ -63,6 +67,13 @@ def lib():
             L.oracle_knn.restype = ctypes.c_int
             L.oracle_pair_scores.argtypes = [P, P, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
             L.oracle_bf_counters.argtypes = [P, P, ctypes.c_void_p, ctypes.c_void_p]
+            L.iib_build.argtypes = [P, ctypes.c_int32]
+            L.iib_build.restype = ctypes.c_void_p
+            L.iib_free.argtypes = [ctypes.c_void_p]
+            L.iib_free.restype = None
+            L.iib_query.argtypes = [ctypes.c_void_p, P, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+            L.iib_query.restype = ctypes.c_int
             _lib = L
     return _lib
 
@@ -151,3 +162,50 @@ def bf_counters(R, S):
     c, a = ctypes.c_int64(0), ctypes.c_int64(0)
     L.oracle_bf_counters(ctypes.byref(hR.c), ctypes.byref(hS.c), ctypes.byref(c), ctypes.byref(a))
     return c.value, a.value
+
+
+def iib_knn(R, S, k: int, rows=None, threads: int = 1, d: int | None = None):
+    """The paper's IIB (Alg. 3) on the host: index S once (single-threaded C), then rows ``rows`` of R (all if
+    None) split over ``threads`` host threads, each running the single-threaded query on its rows.
+    Returns (ids int64 [n, k], scores float64 [n, k], info) with info = {build_s, query_s, visits}."""
+    import time
+    L = lib()
+    hR, hS = _Held(R), _Held(S)
+    d = d if d is not None else S.d
+    t0 = time.perf_counter()
+    ix = L.iib_build(ctypes.byref(hS.c), d)
+    build_s = time.perf_counter() - t0
+    if not ix:
+        raise MemoryError("iib_build allocation failed")
+    try:
+        sel = np.arange(R.n_rows, dtype=np.int64) if rows is None else np.ascontiguousarray(rows, dtype=np.int64)
+        n = len(sel)
+        ids = np.empty((n, k), dtype=np.int64)
+        scores = np.empty((n, k), dtype=np.float64)
+        threads = max(1, min(threads, max(n, 1)))
+        bounds = np.linspace(0, n, threads + 1).astype(np.int64)
+        visits = np.zeros(threads, dtype=np.int64)
+
+        def work(i):
+            a, b = int(bounds[i]), int(bounds[i + 1])
+            if b <= a:
+                return 0
+            sub = sel[a:b]
+            v = ctypes.c_int64(0)
+            rc = L.iib_query(ix, ctypes.byref(hR.c), sub.ctypes.data, b - a, k, ids[a:b].ctypes.data,
+                             scores[a:b].ctypes.data, ctypes.byref(v))
+            visits[i] = v.value
+            return rc
+
+        t1 = time.perf_counter()
+        if threads == 1:
+            rc = [work(0)]
+        else:
+            with ThreadPoolExecutor(threads) as ex:
+                rc = list(ex.map(work, range(threads)))
+        query_s = time.perf_counter() - t1
+        if any(rc):
+            raise MemoryError("iib_query allocation failed")
+        return ids, scores, {"build_s": build_s, "query_s": query_s, "visits": int(visits.sum())}
+    finally:
+        L.iib_free(ix)

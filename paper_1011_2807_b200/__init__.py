@@ -13,6 +13,7 @@ from ._binding import (  # noqa: F401
     Index,
     KnnJoinError,
     knnjoin_build_index,
+    knnjoin_certify,
     knnjoin_index_stats,
     knnjoin_last_error,
     knnjoin_merge,

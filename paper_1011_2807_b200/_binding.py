@@ -40,7 +40,13 @@ class _QueryOptions(ctypes.Structure):
                 ("ev_end", ctypes.c_void_p), ("phase_cycles", ctypes.c_void_p), ("cta_warps", ctypes.c_int32),
                 ("tiles_per_pass", ctypes.c_int32), ("row_order", ctypes.c_int32), ("tile_begin", ctypes.c_int64),
                 ("tile_end", ctypes.c_int64), ("resume_keys", ctypes.c_void_p), ("theta_in", ctypes.c_void_p),
-                ("prune_alpha", ctypes.c_float), ("residual", ctypes.c_int32)]
+                ("prune_alpha", ctypes.c_float), ("residual", ctypes.c_int32), ("precision", ctypes.c_int32),
+                ("row_list", ctypes.c_void_p), ("row_count", ctypes.c_void_p), ("uncertified", ctypes.c_void_p),
+                ("tolerance", ctypes.c_float)]
+
+
+class _MergeOptions(ctypes.Structure):
+    _fields_ = [("float_keys", ctypes.c_int32), ("row_list", ctypes.c_void_p), ("row_count", ctypes.c_void_p)]
 
 
 class _IndexInfo(ctypes.Structure):
@@ -80,9 +86,14 @@ def _load():
     L.knnjoin_query.restype = c.c_int
     L.knnjoin_merge_workspace_bytes.argtypes = [P(_CSR)]
     L.knnjoin_merge_workspace_bytes.restype = c.c_size_t
-    L.knnjoin_merge.argtypes = [c.c_void_p, c.c_int32, P(_CSR), c.c_int32, c.c_int, c.c_int32, c.c_void_p, c.c_void_p,
-                                c.c_void_p, c.c_void_p, c.c_size_t, c.c_void_p]
+    L.knnjoin_merge.argtypes = [c.c_void_p, c.c_int32, P(_CSR), c.c_int32, c.c_int, c.c_int32, P(_MergeOptions),
+                                c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_size_t, c.c_void_p]
     L.knnjoin_merge.restype = c.c_int
+    L.knnjoin_certify_workspace_bytes.argtypes = [P(_CSR)]
+    L.knnjoin_certify_workspace_bytes.restype = c.c_size_t
+    L.knnjoin_certify.argtypes = [c.c_void_p, P(_CSR), c.c_int32, c.c_int, c.c_int32, c.c_float, c.c_void_p, c.c_void_p,
+                                  c.c_size_t, c.c_void_p]
+    L.knnjoin_certify.restype = c.c_int
     L.knnjoin_validate_csr.argtypes = [P(_CSR), c.c_int32, c.c_void_p, P(c.c_int64)]
     L.knnjoin_validate_csr.restype = c.c_int
     L.knnjoin_iiib_profile_bytes.argtypes = [P(_CSR), c.c_int32]
@@ -110,7 +121,7 @@ _lib = _load()
 
 EXPORTS = ["knnjoin_index_bytes", "knnjoin_build_workspace_bytes", "knnjoin_build_index", "knnjoin_index_stats",
            "knnjoin_free_index", "knnjoin_query_workspace_bytes", "knnjoin_query", "knnjoin_merge_workspace_bytes",
-           "knnjoin_merge", "knnjoin_validate_csr", "knnjoin_last_error", "knnjoin_version",
+           "knnjoin_merge", "knnjoin_certify_workspace_bytes", "knnjoin_certify", "knnjoin_validate_csr", "knnjoin_last_error", "knnjoin_version",
            "knnjoin_iiib_profile_bytes", "knnjoin_iiib_profile", "knnjoin_iiib_threshold_workspace_bytes",
            "knnjoin_iiib_threshold", "knnjoin_iiib_split_workspace_bytes", "knnjoin_iiib_split"]
 
@@ -239,12 +250,22 @@ def knnjoin_query(index: Index, R: DeviceCSR, k: int, want_keys: bool = False, w
                   workspace: torch.Tensor | None = None, phase_cycles: torch.Tensor | None = None,
                   cta_warps: int = 0, tiles_per_pass: int = 0, row_order: int = 0, tile_range=(0, 0),
                   resume_keys: torch.Tensor | None = None, theta_in: torch.Tensor | None = None,
-                  prune_alpha: float = 0.0, residual: int = 0):
+                  prune_alpha: float = 0.0, residual: int = 0, precision: int = 0,
+                  row_list: torch.Tensor | None = None, uncertified: torch.Tensor | None = None,
+                  tolerance: float = 0.0, out=None):
     """Returns (ids int32 [n,k], scores float32 [n,k], keys uint64-as-int64 [n,k] or None).
-    tile_range / resume_keys (int64 [n,k]) / theta_in (int64 [n]) / prune_alpha: see knnjoin_query_options."""
+    tile_range / resume_keys (int64 [n,k]) / theta_in (int64 [n]) / prune_alpha / precision / tolerance: see
+    knnjoin_query_options.  row_list: device int32 [1 + m] laid out as knnjoin_certify's list (count, then rows).
+    uncertified: device int32 [1 + n] receiving the certification list.  out: (ids, scores, keys) tensors to
+    write into (rows outside row_list keep their contents)."""
     for t, shape in ((resume_keys, (R.n_rows, k)), (theta_in, (R.n_rows,))):
         if t is not None and (tuple(t.shape) != shape or t.dtype != torch.int64 or not t.is_contiguous()):
             raise ValueError(f"expected a contiguous int64 tensor of shape {shape}")
+    for t in (row_list, uncertified):
+        if t is not None and (t.dtype != torch.int32 or not t.is_contiguous() or t.numel() < 1 or t.device.type != "cuda"):
+            raise ValueError("row_list / uncertified must be contiguous device int32 tensors [1 + rows]")
+    if uncertified is not None and uncertified.numel() < R.n_rows + 1:
+        raise ValueError("uncertified needs 1 + n_rows entries")
     cR = R._c()
     if events and (events[0].cuda_event == 0 or events[1].cuda_event == 0):
         raise ValueError("timing events must have been recorded once (so their cudaEvent handles exist)")
@@ -253,15 +274,24 @@ def knnjoin_query(index: Index, R: DeviceCSR, k: int, want_keys: bool = False, w
                        phase_cycles.data_ptr() if phase_cycles is not None else 0, cta_warps, tiles_per_pass,
                        row_order, tile_range[0], tile_range[1],
                        resume_keys.data_ptr() if resume_keys is not None else 0,
-                       theta_in.data_ptr() if theta_in is not None else 0, prune_alpha, residual)
+                       theta_in.data_ptr() if theta_in is not None else 0, prune_alpha, residual, precision,
+                       row_list.data_ptr() + 4 if row_list is not None else 0,
+                       row_list.data_ptr() if row_list is not None else 0,
+                       uncertified.data_ptr() if uncertified is not None else 0, tolerance)
     wbytes = _lib.knnjoin_query_workspace_bytes(index.handle, ctypes.byref(cR), k, ctypes.byref(qo))
     if wbytes == 0:
         raise KnnJoinError(1, "knnjoin_query_workspace_bytes", knnjoin_last_error())
     dev = R.indptr.device
     n = R.n_rows
-    ids = torch.empty((n, k), dtype=torch.int32, device=dev) if want_ids else None
-    scores = torch.empty((n, k), dtype=torch.float32, device=dev) if want_ids else None
-    keys = torch.empty((n, k), dtype=torch.int64, device=dev) if want_keys else None
+    if out is not None:
+        ids, scores, keys = out
+        for t, dt in ((ids, torch.int32), (scores, torch.float32), (keys, torch.int64)):
+            if t is not None and (tuple(t.shape) != (n, k) or t.dtype != dt or not t.is_contiguous()):
+                raise ValueError("out tensors must be contiguous [n, k] int32 / float32 / int64")
+    else:
+        ids = torch.empty((n, k), dtype=torch.int32, device=dev) if want_ids else None
+        scores = torch.empty((n, k), dtype=torch.float32, device=dev) if want_ids else None
+        keys = torch.empty((n, k), dtype=torch.int64, device=dev) if want_keys else None
     ws = workspace if (workspace is not None and workspace.numel() >= wbytes) else _empty_u8(wbytes, dev)
     _check(_lib.knnjoin_query(index.handle, ctypes.byref(cR), k, ctypes.byref(qo),
                               keys.data_ptr() if keys is not None else 0, ids.data_ptr() if ids is not None else 0,
@@ -272,22 +302,51 @@ def knnjoin_query(index: Index, R: DeviceCSR, k: int, want_keys: bool = False, w
 
 
 def knnjoin_merge(keys: torch.Tensor, R: DeviceCSR, d: int, s_dtype: int, k: int, want_keys: bool = False,
-                  stream=None):
-    """keys: int64 view of uint64 [P, n, k].  Returns (ids, scores, merged keys or None)."""
+                  stream=None, float_keys: int = 0, row_list: torch.Tensor | None = None, out=None):
+    """keys: int64 view of uint64 [P, n, k].  Returns (ids, scores, merged keys or None).
+    float_keys / row_list (device int32 [1 + m]: count, then output rows): knnjoin_merge_options.  out: existing
+    (ids, scores, keys) to write into (with row_list only the listed rows are written)."""
     P = keys.shape[0]
+    n = R.n_rows
+    if keys.dim() != 3 or tuple(keys.shape[1:]) != (n, k) or keys.dtype != torch.int64 or not keys.is_contiguous() \
+            or keys.device != R.indptr.device:
+        raise ValueError(f"keys must be a contiguous int64 tensor [P, {n}, {k}] on {R.indptr.device}")
+    if row_list is not None and (row_list.dtype != torch.int32 or not row_list.is_contiguous() or row_list.numel() < 1):
+        raise ValueError("row_list must be a contiguous device int32 tensor [1 + rows]")
     cR = R._c()
     dev = keys.device
-    n = R.n_rows
     wbytes = _lib.knnjoin_merge_workspace_bytes(ctypes.byref(cR))
     ws = _empty_u8(wbytes, dev)
-    ids = torch.empty((n, k), dtype=torch.int32, device=dev)
-    scores = torch.empty((n, k), dtype=torch.float32, device=dev)
-    out_keys = torch.empty((n, k), dtype=torch.int64, device=dev) if want_keys else None
-    _check(_lib.knnjoin_merge(keys.data_ptr(), P, ctypes.byref(cR), d, s_dtype, k,
+    if out is not None:
+        ids, scores, out_keys = out
+    else:
+        ids = torch.empty((n, k), dtype=torch.int32, device=dev)
+        scores = torch.empty((n, k), dtype=torch.float32, device=dev)
+        out_keys = torch.empty((n, k), dtype=torch.int64, device=dev) if want_keys else None
+    mo = _MergeOptions(float_keys, row_list.data_ptr() + 4 if row_list is not None else 0,
+                       row_list.data_ptr() if row_list is not None else 0)
+    _check(_lib.knnjoin_merge(keys.data_ptr(), P, ctypes.byref(cR), d, s_dtype, k, ctypes.byref(mo),
                               out_keys.data_ptr() if out_keys is not None else 0, ids.data_ptr(), scores.data_ptr(),
                               ws.data_ptr(), ws.numel(), _stream_ptr(stream)), "knnjoin_merge")
     ws.record_stream(torch.cuda.current_stream() if stream is None else stream)
     return ids, scores, out_keys
+
+
+def knnjoin_certify(keys: torch.Tensor, R: DeviceCSR, d: int, s_dtype: int, k: int, tolerance: float = 0.0,
+                    stream=None) -> torch.Tensor:
+    """Certification of complete 32-bit lists (keys int64 [n, k]) -> device int32 [1 + n]: count, then the rows
+    whose lists fail the tolerance rule (knnjoin_certify)."""
+    n = R.n_rows
+    if tuple(keys.shape) != (n, k) or keys.dtype != torch.int64 or not keys.is_contiguous():
+        raise ValueError(f"keys must be a contiguous int64 tensor [{n}, {k}]")
+    cR = R._c()
+    dev = R.indptr.device
+    ws = _empty_u8(_lib.knnjoin_certify_workspace_bytes(ctypes.byref(cR)), dev)
+    out = torch.empty(n + 1, dtype=torch.int32, device=dev)
+    _check(_lib.knnjoin_certify(keys.data_ptr(), ctypes.byref(cR), d, s_dtype, k, tolerance, out.data_ptr(),
+                                ws.data_ptr(), ws.numel(), _stream_ptr(stream)), "knnjoin_certify")
+    ws.record_stream(torch.cuda.current_stream() if stream is None else stream)
+    return out
 
 
 def knnjoin_validate_csr(m: DeviceCSR, d: int, stream=None):

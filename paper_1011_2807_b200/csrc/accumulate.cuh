@@ -15,6 +15,8 @@ struct QP {
   const int32_t* head_slot;  // [d] head slot or -1
   const int32_t* head_feat;  // [kMaxHead + 1]; [kMaxHead] = number of head features
   const uint32_t* head_cols; // [n_tiles * T] head-feature bits per S row
+  const int32_t* gate;       // nullptr, or the index's head count (device): the launch runs only when
+  int32_t gate_heads;        //   (count > 0) == gate_heads (knnjoin_query launches both candidate shapes)
   int32_t d, T;
   int64_t NT;
   int64_t s_id_base;
@@ -174,6 +176,7 @@ __device__ __forceinline__ void red_add_shared(uint32_t addr, uint32_t v) {
 template <int B, int KS, bool SINT8, int NW, bool HEADS, bool PRUNE = false>
 __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_accumulate_topk(QP p) {
   static_assert(!PRUNE || (B == 1 && !HEADS), "pruned instances are one-row and head-free");
+  if (p.gate && ((*p.gate > 0) != (p.gate_heads != 0))) return;  // the other candidate shape runs
   constexpr int NT_ = NW * 32;        // threads per CTA
   constexpr int kCap = kcap(NW);      // runs staged per chunk
   constexpr int IPT = (kCap + NT_ - 1) / NT_;  // staged runs per thread (the last may be partial)
@@ -392,8 +395,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
             pk[it] = ((uint64_t)(U[it] > 0) << 32) | U[it];
             mine += pk[it];
           }
-          // U_N of this tile (read after the accumulate); f1: 2^31 > any score, i.e. complete every touched s
-          if (PRUNE && c0 == 0 && tid == 0) s_misc[4] = p.residual ? (int)0x80000000u : 0;
+          // U_N of this tile (read after the accumulate; f1 completes every touched s whatever U_N)
+          if (PRUNE && c0 == 0 && tid == 0) s_misc[4] = 0;
           uint64_t total;
           uint64_t ex = block_exclusive_scan_u64<NW>(mine, s_warp, &total);
           if (PRUNE && un_mine) atomicAdd((unsigned*)&s_misc[4], un_mine);
@@ -573,7 +576,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
           for (int b = 0; b < B; ++b) t32[b] = t32_of(th[b]);
           const uint32_t a0 = acc_s + (uint32_t)(cbase + lane * 4) * 4u;
           // a6: U_N of this tile (0 when nothing was skipped: the plain filter)
-          const uint32_t un = PRUNE ? (uint32_t)s_misc[4] : 0u;
+          const uint32_t un = PRUNE ? (uint32_t)s_misc[4] : 0u;  // <= budget < theta: x + un cannot wrap
+          const bool all_touched = PRUNE && p.residual;           // f1: complete every s with x != 0
           // a6 exact completion of s = local column col: add r's non-essential features that s has, merging s's
           // forward row against the row's runs (both ascending by feature)
           auto complete = [&](uint32_t col) -> uint32_t {
@@ -614,16 +618,17 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
                 const uint4 x = lds_v4(a);
                 sts_v4_zero(a);
                 const uint32_t mx = max(max(x.x, x.y), max(x.z, x.w));
-                if (__any_sync(0xffffffffu, PRUNE ? (mx != 0u && mx + un >= t32[b]) : mx >= t32[b])) {
+                if (__any_sync(0xffffffffu, PRUNE ? (mx != 0u && (all_touched || mx + un >= t32[b])) : mx >= t32[b])) {
                   th[b] = row_theta(b);
                   const uint32_t g0 = gbase + (uint32_t)(cbase + c + lane * 4);
                   uint32_t xv[4] = {x.x, x.y, x.z, x.w};
                   if constexpr (PRUNE) {
-                    if (un) {
+                    if (un || all_touched) {
                       const uint32_t tc = t32_of(th[b]);
 #pragma unroll
                       for (int j = 0; j < 4; ++j)
-                        if (xv[j] != 0u && xv[j] + un >= tc) xv[j] += complete((uint32_t)(cbase + c + lane * 4 + j));
+                        if (xv[j] != 0u && (all_touched || xv[j] + un >= tc))
+                          xv[j] += complete((uint32_t)(cbase + c + lane * 4 + j));
                     }
                   }
 #pragma unroll

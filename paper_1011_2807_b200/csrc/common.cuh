@@ -11,6 +11,8 @@
 
 #define KJ_API extern "C" __attribute__((visibility("default")))
 
+struct knnjoin_index;
+
 namespace kj {
 
 constexpr int kMaxK = 256;
@@ -31,7 +33,7 @@ __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a -
 // host-side layout of the index storage (all offsets 256-byte aligned)
 struct IndexLayout {
   int64_t n_tiles = 0, n_off = 0, unit_cap = 0;
-  size_t off_at = 0, df_at = 0, head_slot_at = 0, head_feat_at = 0, head_cols_at = 0, ids_at = 0, vals_at = 0,
+  size_t off_at = 0, df_at = 0, head_slot_at = 0, head_feat_at = 0, head_cols_at = 0, ids_at = 0, vals_at = 0, wmax_at = 0,
          fwd_ptr_at = 0, fwd_idx_at = 0, fwd_val_at = 0, fmax_at = 0, total = 0;
 };
 // prune: also reserve S's forward rows and (INT8 S) the per-feature maximum weight (pruned queries, a6)
@@ -43,7 +45,9 @@ int32_t resolve_tile(const knnjoin_options* opt);
 
 // per-row score scale: sigma[r] = 2^30 / (sum_d r_d * smax) for FP32 R,
 // 1 for integer R.  inv_sigma[r] = 1 / sigma[r] converts a fixed-point sum back to a score.
-void launch_row_scale(const knnjoin_csr* R, int32_t d, int32_t smax, double* sigma, double* inv_sigma,
+// err (optional): E_r = smax * sum_{d in r} |q_d - r_d sigma_r|, the bound on the absolute error of any pair's
+// fixed-point score (certification in wide.cu)
+void launch_row_scale(const knnjoin_csr* R, int32_t d, int32_t smax, double* sigma, double* inv_sigma, double* err,
                       cudaStream_t st);
 
 // finalize / merge helpers implemented in merge.cu
@@ -51,6 +55,24 @@ int ks_for_k(int32_t k);
 // K4: rank merge of P sorted key lists per row ([P][n][k], disjoint S ids) into the outputs
 cudaError_t launch_merge_keys(const uint64_t* keys, int32_t P, int64_t n, int32_t k, const double* inv_sigma,
                               uint64_t* out_keys, int32_t* out_ids, float* out_scores, cudaStream_t st);
+// float_keys: scores are fp32 bits (wide queries); row_list/row_count: position i -> output row row_list[i]
+cudaError_t launch_merge_keys_ex(const uint64_t* keys, int32_t P, int64_t n, int32_t k, const double* inv_sigma,
+                                 int float_keys, const int32_t* row_list, const int32_t* row_count, int keys_by_row,
+                                 uint64_t* out_keys, int32_t* out_ids, float* out_scores, cudaStream_t st);
+// 64-bit fixed-point queries (wide.cu)
+size_t wide_part_bytes(int32_t k, int64_t n_tiles, int sms, int32_t* G_out);
+cudaError_t launch_wide(const knnjoin_index* idx, const knnjoin_csr* R, int32_t k, int64_t t0, int64_t t1,
+                        const int32_t* row_list, const int32_t* row_count, const uint64_t* resume,
+                        const uint64_t* theta_in, double* sigma64, double* inv64, uint32_t* item_counter,
+                        uint64_t* part_keys, int32_t G, unsigned long long* counters, uint64_t* out_keys,
+                        int32_t* out_ids, float* out_scores, int sms, cudaStream_t st);
+// K4 for the split-mode lists of one candidate shape (gate as in the accumulate kernel)
+cudaError_t launch_merge_keys_gated(const uint64_t* keys, int32_t P, int64_t n, int32_t k, const double* inv_sigma,
+                                    const int32_t* gate, int gate_heads, uint64_t* out_keys, int32_t* out_ids,
+                                    float* out_scores, cudaStream_t st);
+cudaError_t launch_certify(const uint64_t* keys, const double* err, int64_t n, int32_t k, double tau, int32_t* list,
+                           cudaStream_t st);
+constexpr double kDefaultTolerance = 1e-5;  // BASELINE.json north_star: fp32 scores within 1e-5 relative
 
 }  // namespace kj
 
@@ -61,14 +83,15 @@ struct knnjoin_index {
   knnjoin_dtype s_dtype = KNNJOIN_BINARY;
   uint32_t head_min_df = 0xFFFFFFFFu;  // df threshold of head features (0xFFFFFFFF: none)
   int32_t head_max = 0;                // cap on head features (0: none)
-  mutable int32_t n_head_host = -1;    // head count, read once by the first auto-shaped query (-1 unknown)
   const uint32_t* off = nullptr;       // [n_off] posting-unit (16 B) offsets, feature-major: f*(n_tiles+1)+t
   const int32_t* df = nullptr;         // [d] |I_d| (document frequency of each feature in S)
   const int32_t* head_slot = nullptr;  // [d] head slot of a feature, -1 if not a head feature
   const int32_t* head_feat = nullptr;  // [kMaxHead + 1] feature of each head slot (-1 unused); [kMaxHead] = n_head
   const uint32_t* head_cols = nullptr; // [n_tiles * tile] bit i: S row has head feature head_feat[i]
   const uint16_t* ids = nullptr;       // [unit_cap*8] local S ids (< tile); padding = tile + (u mod 32)
-  const uint8_t* vals = nullptr;       // [unit_cap*8] INT8 S weights (nullptr for BINARY S)
+  const uint8_t* vals = nullptr;       // [unit_cap*8] INT8 S weights (nullptr for BINARY / FP32 S)
+  const uint32_t* vals32 = nullptr;    // [unit_cap*8] FP32 S weight bits (FP32 S only; queried at 64 bits, wide.cu)
+  const uint32_t* wmax = nullptr;      // [1] largest S weight: u32 (BINARY 1, INT8) or float bits (FP32)
   // pruned mode (options.prune = 1): forward rows of S (local row ids) and per-feature max weight
   int32_t prune = 0;
   float alpha = 0.0f;                  // default alpha of pruned queries

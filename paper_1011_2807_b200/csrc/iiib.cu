@@ -263,7 +263,7 @@ KJ_API knnjoin_status knnjoin_iiib_threshold(const uint64_t* keys, const knnjoin
   double* sigma = (double*)workspace;
   double* inv = sigma + (R->n_rows > 0 ? R->n_rows : 1);
   // the per-row scale of knnjoin_query (smax = 127 for INT8 S, 1 for BINARY S)
-  launch_row_scale(R, d, s_dtype == KNNJOIN_INT8 ? 127 : 1, sigma, inv, st);
+  launch_row_scale(R, d, s_dtype == KNNJOIN_INT8 ? 127 : 1, sigma, inv, nullptr, st);
   k_iiib_threshold<<<1, 1024, 0, st>>>(keys, R->n_rows, k, inv, out2);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "iiib threshold");

@@ -66,6 +66,9 @@ bool index_layout(const knnjoin_csr* S, int32_t d, int32_t tile, bool prune, Ind
   at = align_up(at + 16 * (size_t)L->unit_cap, 256);
   L->vals_at = at;
   if (S->dtype == KNNJOIN_INT8) at = align_up(at + 8 * (size_t)L->unit_cap, 256);
+  if (S->dtype == KNNJOIN_FP32) at = align_up(at + 32 * (size_t)L->unit_cap, 256);  // fp32 weights, 8 per unit
+  L->wmax_at = at;  // largest S weight (u32 for BINARY / INT8, float bits for FP32)
+  at = align_up(at + 4, 256);
   L->fwd_ptr_at = L->fwd_idx_at = L->fwd_val_at = L->fmax_at = at;
   if (prune) {
     L->fwd_ptr_at = at;
@@ -97,9 +100,13 @@ int end_bit_for(int64_t max_key) {
 bool build_ws_layout(const knnjoin_csr* S, int32_t d, const IndexLayout& L, BuildWs* W) {
   size_t nnz = (size_t)S->nnz, n_off = (size_t)L.n_off;
   size_t sort_bytes = 0, scan_bytes = 0;
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)nnz, 0,
-                                                  end_bit_for(L.n_off - 1));
+  cudaError_t e = S->dtype == KNNJOIN_FP32
+                      ? cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                                        (const uint64_t*)nullptr, (uint64_t*)nullptr, (int)nnz, 0,
+                                                        end_bit_for(L.n_off - 1))
+                      : cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                                        (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)nnz, 0,
+                                                        end_bit_for(L.n_off - 1));
   if (e != cudaSuccess) return false;
   e = cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n_off);
   if (e != cudaSuccess) return false;
@@ -109,8 +116,10 @@ bool build_ws_layout(const knnjoin_csr* S, int32_t d, const IndexLayout& L, Buil
   W->first_at = at;  at = align_up(at + 4 * n_off, 256);
   W->ka_at = at;     at = align_up(at + 4 * nnz, 256);
   W->kb_at = at;     at = align_up(at + 4 * nnz, 256);
-  W->va_at = at;     at = align_up(at + 4 * nnz, 256);
-  W->vb_at = at;     at = align_up(at + 4 * nnz, 256);
+  // sort values: (local id | int8 weight << 16) as u32, or (local id | fp32 weight bits << 32) as u64 (FP32 S)
+  const size_t vb = S->dtype == KNNJOIN_FP32 ? 8 : 4;
+  W->va_at = at;     at = align_up(at + vb * nnz, 256);
+  W->vb_at = at;     at = align_up(at + vb * nnz, 256);
   W->cub_at = at;
   W->cub_bytes = sort_bytes;
   if (scan_bytes > W->cub_bytes) W->cub_bytes = scan_bytes;
@@ -124,8 +133,12 @@ bool check_build_args(const knnjoin_csr* S, int32_t d, const knnjoin_options* op
   if (d <= 0) { set_error("d must be > 0 (got %d)", d); return false; }
   if (d >= (1 << 24)) { set_error("d must be < 2^24 (feature ids share a word with an 8-row mask)"); return false; }
   if (S->n_rows < 0 || S->nnz < 0) { set_error("negative S size"); return false; }
-  if (S->dtype != KNNJOIN_BINARY && S->dtype != KNNJOIN_INT8) {
-    set_error("S dtype %d unsupported: S must be BINARY or INT8 (DESIGN.md: fixed-point scores)", (int)S->dtype);
+  if (S->dtype != KNNJOIN_BINARY && S->dtype != KNNJOIN_INT8 && S->dtype != KNNJOIN_FP32) {
+    set_error("bad S dtype %d", (int)S->dtype);
+    return false;
+  }
+  if (S->dtype == KNNJOIN_FP32 && opt && opt->prune) {
+    set_error("FP32 S is queried at 64-bit fixed point only: prune = 1 (a6 / f1) needs BINARY or INT8 S");
     return false;
   }
   if (S->nnz >= ((int64_t)1 << 31)) { set_error("nnz(S) must be < 2^31 per index (shard S)"); return false; }
@@ -152,10 +165,11 @@ bool check_build_args(const knnjoin_csr* S, int32_t d, const knnjoin_options* op
   return true;
 }
 
-// warp per S row
+// warp per S row.  Sort value: local id | weight << 16 (VT = u32: BINARY / INT8) or | fp32 bits << 32 (VT = u64)
+template <typename VT>
 __global__ void k_keys(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                       const int8_t* __restrict__ values, int64_t n_s, int32_t d, int32_t tile, int64_t n_tiles,
-                       uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, uint32_t sentinel_key) {
+                       const void* __restrict__ values, int64_t n_s, int32_t d, int32_t tile, int64_t n_tiles,
+                       uint32_t* __restrict__ keys, VT* __restrict__ vals, uint32_t sentinel_key) {
   int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (row >= n_s) return;
@@ -165,7 +179,10 @@ __global__ void k_keys(const int64_t* __restrict__ indptr, const int32_t* __rest
     int32_t f = indices[j];
     if (f >= 0 && f < d) {
       keys[j] = (uint32_t)((int64_t)f * (n_tiles + 1) + t);
-      vals[j] = local | ((values ? (uint32_t)(uint8_t)values[j] : 0u) << 16);
+      if constexpr (sizeof(VT) == 8)
+        vals[j] = (VT)local | ((VT)__float_as_uint(((const float*)values)[j]) << 32);
+      else
+        vals[j] = local | ((values ? (uint32_t)(uint8_t)((const int8_t*)values)[j] : 0u) << 16);
     } else {
       keys[j] = sentinel_key;
       vals[j] = 0;
@@ -297,10 +314,11 @@ __global__ void k_fill_pads(uint4* __restrict__ ids, int64_t units, uint32_t til
 }
 
 // posting of sorted rank rho goes to position rho of its slice (k_block_layout permutes inside full blocks)
-__global__ void k_scatter(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, int64_t nnz,
+template <typename VT, typename WT>
+__global__ void k_scatter(const uint32_t* __restrict__ keys, const VT* __restrict__ vals, int64_t nnz,
                           const uint32_t* __restrict__ off, const uint32_t* __restrict__ first,
                           const uint32_t* __restrict__ units, uint32_t sentinel_key, uint16_t* __restrict__ ids,
-                          uint8_t* __restrict__ wvals) {
+                          WT* __restrict__ wvals) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nnz) return;
   uint32_t key = keys[i];
@@ -313,17 +331,18 @@ __global__ void k_scatter(const uint32_t* __restrict__ keys, const uint32_t* __r
   uint32_t dst = rho;
   if (nfull == 0) dst = (rho % m) * 8 + rho / m;  // short slice (one partial block): transpose here
   const size_t pos = (size_t)off[key] * 8 + dst;
-  const uint32_t v = vals[i];
+  const VT v = vals[i];
   ids[pos] = (uint16_t)(v & 0xFFFFu);
-  if (wvals) wvals[pos] = (uint8_t)(v >> 16);
+  if (wvals) wvals[pos] = sizeof(VT) == 8 ? (WT)(v >> 32) : (WT)(v >> 16);
 }
 
 // Warp per slice of at least 32 units (grid-stride over keys; shorter slices were transposed by k_scatter):
 // every block of m <= 32 units, stable counting sort by bank (id mod 32; padding last): rank r -> position r
 // (unit r/8, slot r%8).  Deterministic: ranks come from slot-ordered
 // match_any passes, not from the order of atomics.
+template <typename WT>
 __global__ void k_block_layout(const uint32_t* __restrict__ off, const uint32_t* __restrict__ units, int64_t n_keys,
-                               uint32_t tile, uint16_t* __restrict__ ids, uint8_t* __restrict__ wvals) {
+                               uint32_t tile, uint16_t* __restrict__ ids, WT* __restrict__ wvals) {
   __shared__ uint32_t s_cnt[8][33];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint32_t* cnt = s_cnt[wib];
@@ -339,7 +358,7 @@ __global__ void k_block_layout(const uint32_t* __restrict__ off, const uint32_t*
       const uint32_t m = min(32u, U - 32u * blk);
       const size_t b0 = base + (size_t)blk * 256;
       uint16_t id[8];
-      uint8_t w[8];
+      WT w[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) { id[j] = 0xFFFF; w[j] = 0; }
       if (lane < (int)m) {
@@ -348,9 +367,8 @@ __global__ void k_block_layout(const uint32_t* __restrict__ off, const uint32_t*
 #pragma unroll
         for (int j = 0; j < 8; ++j) id[j] = (uint16_t)(xs[j >> 1] >> (16 * (j & 1)));
         if (wvals) {
-          const uint2 y = *(const uint2*)(wvals + b0 + 8 * lane);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) w[j] = (uint8_t)((j < 4 ? y.x : y.y) >> (8 * (j & 3)));
+          for (int j = 0; j < 8; ++j) w[j] = wvals[b0 + 8 * lane + j];
         }
       }
       // stable counting sort by bank (bucket 32 = padding, after every real posting; bucket 33 = lanes past
@@ -433,6 +451,16 @@ __global__ void k_fmax(const int32_t* __restrict__ indices, const int8_t* __rest
   if (f >= 0 && f < d) atomicMax(&fmax[f], (uint32_t)(uint8_t)values[i]);
 }
 
+// the largest weight of S (u32 for INT8; float bits for FP32 -- positive floats order like their bits): the
+// 64-bit fixed-point scale of wide queries (wide.cu) keeps every partial score below 2^62 with it
+__global__ void k_wmax(const void* __restrict__ values, knnjoin_dtype dt, int64_t nnz, uint32_t* __restrict__ wmax) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t v = 0;
+  if (i < nnz) v = dt == KNNJOIN_FP32 ? __float_as_uint(((const float*)values)[i]) : (uint32_t)(uint8_t)((const int8_t*)values)[i];
+  v = __reduce_max_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0 && v) atomicMax(wmax, v);
+}
+
 }  // namespace
 
 // minimum df of a head feature (0xFFFFFFFF = no heads); BINARY S only
@@ -476,13 +504,12 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   *out = nullptr;
   int32_t tile;
   if (!check_build_args(S, d, opt, &tile)) return (S && d <= 0) ? KNNJOIN_ERR_DIM : KNNJOIN_ERR_ARG;
-  if (S->dtype != KNNJOIN_BINARY && S->dtype != KNNJOIN_INT8) return KNNJOIN_ERR_UNSUPPORTED;
   if (s_id_base < 0 || s_id_base + S->n_rows > (int64_t)0x7FFFFFFF) {
     set_error("global S ids must fit in int32 (s_id_base + n_rows < 2^31)");
     return KNNJOIN_ERR_UNSUPPORTED;
   }
   if (S->n_rows > 0 && (!S->indptr || (S->nnz > 0 && !S->indices))) { set_error("S pointers are NULL"); return KNNJOIN_ERR_ARG; }
-  if (S->dtype == KNNJOIN_INT8 && S->nnz > 0 && !S->values) { set_error("INT8 S needs values"); return KNNJOIN_ERR_ARG; }
+  if (S->dtype != KNNJOIN_BINARY && S->nnz > 0 && !S->values) { set_error("INT8 / FP32 S needs values"); return KNNJOIN_ERR_ARG; }
   IndexLayout L;
   BuildWs W;
   if (!index_layout(S, d, tile, opt && opt->prune, &L, opt ? opt->forward : nullptr) || !build_ws_layout(S, d, L, &W)) { set_error("layout failed"); return KNNJOIN_ERR_ARG; }
@@ -500,6 +527,9 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   uint32_t* head_cols = (uint32_t*)(sb + L.head_cols_at);
   uint16_t* ids = (uint16_t*)(sb + L.ids_at);
   uint8_t* vals = S->dtype == KNNJOIN_INT8 ? (uint8_t*)(sb + L.vals_at) : nullptr;
+  uint32_t* vals32 = S->dtype == KNNJOIN_FP32 ? (uint32_t*)(sb + L.vals_at) : nullptr;  // fp32 weight bits
+  uint32_t* wmax = (uint32_t*)(sb + L.wmax_at);
+  const bool f32 = S->dtype == KNNJOIN_FP32;
   uint32_t* counts = (uint32_t*)(wb + W.counts_at);
   uint32_t* units = (uint32_t*)(wb + W.units_at);
   uint32_t* first = (uint32_t*)(wb + W.first_at);
@@ -507,6 +537,8 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   uint32_t* kb = (uint32_t*)(wb + W.kb_at);
   uint32_t* va = (uint32_t*)(wb + W.va_at);
   uint32_t* vb = (uint32_t*)(wb + W.vb_at);
+  uint64_t* va64 = (uint64_t*)va;
+  uint64_t* vb64 = (uint64_t*)vb;
   void* cubtmp = wb + W.cub_at;
   const uint32_t sentinel_key = (uint32_t)(L.n_off - 1);
   const uint32_t min_df = head_min_df(S, opt);
@@ -518,15 +550,28 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   if ((e = cudaMemsetAsync(head_slot, 0xFF, 4 * (size_t)d, st)) != cudaSuccess) return cuda_fail(e, "memset head_slot");
   if ((e = cudaMemsetAsync(head_cols, 0, 4 * (size_t)L.n_tiles * tile, st)) != cudaSuccess) return cuda_fail(e, "memset head_cols");
   if (vals && (e = cudaMemsetAsync(vals, 0, 8 * (size_t)L.unit_cap, st)) != cudaSuccess) return cuda_fail(e, "memset vals");
+  if (vals32 && (e = cudaMemsetAsync(vals32, 0, 32 * (size_t)L.unit_cap, st)) != cudaSuccess) return cuda_fail(e, "memset vals");
+  if ((e = cudaMemsetAsync(wmax, 0, 4, st)) != cudaSuccess) return cuda_fail(e, "memset wmax");
+  if (S->dtype == KNNJOIN_BINARY) {
+    if ((e = cudaMemsetAsync(wmax, 0x01, 1, st)) != cudaSuccess) return cuda_fail(e, "wmax");  // weight 1
+  } else if (S->nnz > 0) {
+    k_wmax<<<(unsigned)((S->nnz + 255) / 256), 256, 0, st>>>(S->values, S->dtype, S->nnz, wmax);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_wmax");
+  }
   const unsigned gnnz = (unsigned)((S->nnz + 255) / 256);
   if (S->nnz > 0) {
     int64_t threads = S->n_rows * 32;
-    k_keys<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(S->indptr, S->indices, (const int8_t*)S->values,
-                                                            S->n_rows, d, tile, L.n_tiles, ka, va, sentinel_key);
+    if (f32)
+      k_keys<uint64_t><<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(S->indptr, S->indices, S->values, S->n_rows, d,
+                                                                        tile, L.n_tiles, ka, va64, sentinel_key);
+    else
+      k_keys<uint32_t><<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(S->indptr, S->indices, S->values, S->n_rows, d,
+                                                                        tile, L.n_tiles, ka, va, sentinel_key);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_keys");
     size_t tb = W.cub_bytes;
-    if ((e = cub::DeviceRadixSort::SortPairs(cubtmp, tb, ka, kb, va, vb, (int)S->nnz, 0, end_bit_for(L.n_off - 1), st)) != cudaSuccess)
-      return cuda_fail(e, "radix sort");
+    e = f32 ? cub::DeviceRadixSort::SortPairs(cubtmp, tb, ka, kb, va64, vb64, (int)S->nnz, 0, end_bit_for(L.n_off - 1), st)
+            : cub::DeviceRadixSort::SortPairs(cubtmp, tb, ka, kb, va, vb, (int)S->nnz, 0, end_bit_for(L.n_off - 1), st);
+    if (e != cudaSuccess) return cuda_fail(e, "radix sort");
     k_seg_first<<<gnnz, 256, 0, st>>>(kb, S->nnz, sentinel_key, first);
     k_seg_count<<<gnnz, 256, 0, st>>>(kb, S->nnz, sentinel_key, first, counts);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_seg");
@@ -543,7 +588,10 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   k_fill_pads<<<(unsigned)((L.unit_cap + 255) / 256), 256, 0, st>>>((uint4*)ids, L.unit_cap, (uint32_t)tile);
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_fill_pads");
   if (S->nnz > 0) {
-    k_scatter<<<gnnz, 256, 0, st>>>(kb, vb, S->nnz, off, first, units, sentinel_key, ids, vals);
+    if (f32)
+      k_scatter<<<gnnz, 256, 0, st>>>(kb, vb64, S->nnz, off, first, units, sentinel_key, ids, vals32);
+    else
+      k_scatter<<<gnnz, 256, 0, st>>>(kb, vb, S->nnz, off, first, units, sentinel_key, ids, vals);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_scatter");
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -551,7 +599,10 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
     const int64_t want = (L.n_off - 1 + 7) / 8;
     const int64_t cap = (int64_t)sms * 16;
     const unsigned grid = (unsigned)(want < cap ? (want > 0 ? want : 1) : cap);
-    k_block_layout<<<grid, 256, 0, st>>>(off, units, L.n_off - 1, (uint32_t)tile, ids, vals);
+    if (f32)
+      k_block_layout<<<grid, 256, 0, st>>>(off, units, L.n_off - 1, (uint32_t)tile, ids, vals32);
+    else
+      k_block_layout<<<grid, 256, 0, st>>>(off, units, L.n_off - 1, (uint32_t)tile, ids, vals);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_block_layout");
     if (head_max > 0) {
       int64_t threads = S->n_rows * 32;
@@ -605,7 +656,6 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   h->s_dtype = S->dtype;
   h->head_min_df = min_df;
   h->head_max = head_max;
-  if (head_max == 0) h->n_head_host = 0;  // no head features: known without reading the device
   h->off = off;
   h->df = df;
   h->head_slot = head_slot;
@@ -613,6 +663,8 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   h->head_cols = head_cols;
   h->ids = ids;
   h->vals = vals;
+  h->vals32 = vals32;
+  h->wmax = wmax;
   h->prune = prune ? 1 : 0;
   h->alpha = prune ? (opt->alpha > 0.0f ? opt->alpha : kDefaultPruneAlpha) : 0.0f;
   h->fwd_ptr = fwd_ptr;

@@ -37,13 +37,21 @@ namespace {
 // Warp per row.  The P lists of a row are sorted (descending, zero padding last) and hold distinct keys
 // (disjoint S id ranges), so the merged position of a key is its position in its own list plus the number of
 // larger keys in the other P-1 lists (binary searches); positions past the row's positive keys are padding.
+// float_keys: the score field is fp32 bits of the score (64-bit fixed-point queries, wide.cu), else a 32-bit
+// fixed-point sum decoded with inv_sigma.  row_list / row_count: list position i holds output row row_list[i]
+// (only the first *row_count positions are merged); nullptr: position i is row i.  keys_by_row: the lists of
+// listed row r sit at slab position r (a [P][n][k] gather of whole-R outputs), else at list position i.
 __global__ void k_merge(const uint64_t* __restrict__ keys, int32_t P, int64_t n, int32_t k,
-                        const double* __restrict__ inv_sigma, uint64_t* out_keys, int32_t* out_ids,
-                        float* out_scores) {
-  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+                        const double* __restrict__ inv_sigma, int float_keys, const int32_t* __restrict__ row_list,
+                        const int32_t* __restrict__ row_count, int keys_by_row, const int32_t* __restrict__ gate,
+                        int gate_heads, uint64_t* out_keys, int32_t* out_ids, float* out_scores) {
+  if (gate && ((*gate > 0) != (gate_heads != 0))) return;
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (r >= n) return;
-  auto list = [&](int pr) { return keys + ((size_t)pr * n + r) * k; };
+  if (i >= n || (row_count && i >= (int64_t)*row_count)) return;
+  const int64_t r = row_list ? (int64_t)row_list[i] : i;
+  const int64_t at = keys_by_row ? r : i;
+  auto list = [&](int pr) { return keys + ((size_t)pr * n + at) * k; };
   auto count_gt = [&](const uint64_t* lst, uint64_t x) {
     int lo = 0, hi = k;
     while (lo < hi) {
@@ -62,11 +70,11 @@ __global__ void k_merge(const uint64_t* __restrict__ keys, int32_t P, int64_t n,
     } else {
       if (out_keys) out_keys[o] = key;
       if (out_ids) out_ids[o] = (int32_t)(0xFFFFFFFFu - (uint32_t)key);
-      if (out_scores) out_scores[o] = (float)((double)score * inv_sigma[r]);
+      if (out_scores) out_scores[o] = float_keys ? __uint_as_float(score) : (float)((double)score * inv_sigma[r]);
     }
   };
-  for (int i = lane; i < P * k; i += 32) {
-    const int pr = i / k, pos = i % k;
+  for (int e = lane; e < P * k; e += 32) {
+    const int pr = e / k, pos = e % k;
     const uint64_t x = __ldg((const unsigned long long*)list(pr) + pos);
     if (x == 0) continue;
     int rank = pos;
@@ -81,12 +89,29 @@ __global__ void k_merge(const uint64_t* __restrict__ keys, int32_t P, int64_t n,
 
 }  // namespace
 
-cudaError_t launch_merge_keys(const uint64_t* keys, int32_t P, int64_t n, int32_t k, const double* inv_sigma,
-                              uint64_t* out_keys, int32_t* out_ids, float* out_scores, cudaStream_t st) {
+cudaError_t launch_merge_keys_ex(const uint64_t* keys, int32_t P, int64_t n, int32_t k, const double* inv_sigma,
+                                 int float_keys, const int32_t* row_list, const int32_t* row_count, int keys_by_row,
+                                 uint64_t* out_keys, int32_t* out_ids, float* out_scores, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const int64_t threads = n * 32;
-  k_merge<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(keys, P, n, k, inv_sigma, out_keys, out_ids, out_scores);
+  k_merge<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(keys, P, n, k, inv_sigma, float_keys, row_list, row_count,
+                                                             keys_by_row, nullptr, 0, out_keys, out_ids, out_scores);
   return cudaGetLastError();
+}
+
+cudaError_t launch_merge_keys_gated(const uint64_t* keys, int32_t P, int64_t n, int32_t k, const double* inv_sigma,
+                                    const int32_t* gate, int gate_heads, uint64_t* out_keys, int32_t* out_ids,
+                                    float* out_scores, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t threads = n * 32;
+  k_merge<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(keys, P, n, k, inv_sigma, 0, nullptr, nullptr, 0, gate,
+                                                             gate_heads, out_keys, out_ids, out_scores);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_merge_keys(const uint64_t* keys, int32_t P, int64_t n, int32_t k, const double* inv_sigma,
+                              uint64_t* out_keys, int32_t* out_ids, float* out_scores, cudaStream_t st) {
+  return launch_merge_keys_ex(keys, P, n, k, inv_sigma, 0, nullptr, nullptr, 0, out_keys, out_ids, out_scores, st);
 }
 
 namespace {
@@ -131,11 +156,17 @@ KJ_API size_t knnjoin_merge_workspace_bytes(const knnjoin_csr* R) {
 }
 
 KJ_API knnjoin_status knnjoin_merge(const uint64_t* keys, int32_t P, const knnjoin_csr* R, int32_t d,
-                                    knnjoin_dtype s_dtype, int32_t k, uint64_t* out_keys, int32_t* out_ids, float* out_scores,
+                                    knnjoin_dtype s_dtype, int32_t k, const knnjoin_merge_options* mopt,
+                                    uint64_t* out_keys, int32_t* out_ids, float* out_scores,
                                     void* workspace, size_t workspace_bytes, void* stream) {
   if (!R || P < 1 || k < 1 || k > kMaxK) { set_error("bad merge arguments (P %d, k %d)", P, k); return KNNJOIN_ERR_ARG; }
   if (!out_keys && !out_ids && !out_scores) { set_error("no output"); return KNNJOIN_ERR_ARG; }
-  if (s_dtype != KNNJOIN_BINARY && s_dtype != KNNJOIN_INT8) { set_error("S dtype must be BINARY or INT8"); return KNNJOIN_ERR_UNSUPPORTED; }
+  if (s_dtype != KNNJOIN_BINARY && s_dtype != KNNJOIN_INT8 && s_dtype != KNNJOIN_FP32) { set_error("bad S dtype"); return KNNJOIN_ERR_ARG; }
+  const int float_keys = (s_dtype == KNNJOIN_FP32 || (mopt && mopt->float_keys)) ? 1 : 0;
+  if (mopt && (mopt->row_list != nullptr) != (mopt->row_count != nullptr)) {
+    set_error("row_list and row_count go together");
+    return KNNJOIN_ERR_ARG;
+  }
   size_t need = knnjoin_merge_workspace_bytes(R);
   if (!workspace || workspace_bytes < need) { set_error("merge workspace %zu < %zu", workspace_bytes, need); return KNNJOIN_ERR_WORKSPACE; }
   if (R->n_rows == 0) return KNNJOIN_OK;
@@ -143,10 +174,11 @@ KJ_API knnjoin_status knnjoin_merge(const uint64_t* keys, int32_t P, const knnjo
   cudaStream_t st = (cudaStream_t)stream;
   double* inv = (double*)workspace;
   if (d <= 0) { set_error("d must be > 0"); return KNNJOIN_ERR_DIM; }
-  launch_row_scale(R, d, s_dtype == KNNJOIN_INT8 ? 127 : 1, nullptr, inv, st);
+  if (!float_keys) launch_row_scale(R, d, s_dtype == KNNJOIN_INT8 ? 127 : 1, nullptr, inv, nullptr, st);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "row scale");
-  if ((e = launch_merge_keys(keys, P, R->n_rows, k, inv, out_keys, out_ids, out_scores, st)) != cudaSuccess)
+  if ((e = launch_merge_keys_ex(keys, P, R->n_rows, k, inv, float_keys, mopt ? mopt->row_list : nullptr,
+                                mopt ? mopt->row_count : nullptr, 1, out_keys, out_ids, out_scores, st)) != cudaSuccess)
     return cuda_fail(e, "k_merge");
   return KNNJOIN_OK;
 }

@@ -29,7 +29,8 @@ namespace {
 // ------------------------------------------------------------------------------------------- a3 prep
 __global__ void k_row_scale_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                                    const float* __restrict__ values, int64_t n, int32_t d, int32_t smax,
-                                   double* __restrict__ sigma, double* __restrict__ inv_sigma) {
+                                   double* __restrict__ sigma, double* __restrict__ inv_sigma,
+                                   double* __restrict__ err) {
   int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (row >= n) return;
@@ -40,11 +41,26 @@ __global__ void k_row_scale_kernel(const int64_t* __restrict__ indptr, const int
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   }
+  double sg = 1.0;
+  if (values && s > 0.0) sg = kFixedOne / (s * (double)smax);
   if (lane == 0) {
-    double sg = 1.0;
-    if (values && s > 0.0) sg = kFixedOne / (s * (double)smax);
     if (sigma) sigma[row] = sg;
     if (inv_sigma) inv_sigma[row] = 1.0 / sg;
+  }
+  if (err) {  // E_r = smax * sum_d |q_d - r_d sigma_r|, q_d exactly as quantize() rounds it (0 for integer R)
+    double e = 0.0;
+    if (values) {
+      for (int64_t j = indptr[row] + lane; j < indptr[row + 1]; j += 32)
+        if (indices[j] < d) {
+          const double x = (double)values[j] * sg;
+          int32_t q = (int32_t)rint(x);
+          q = q < 1 ? 1 : q;
+          e += fabs((double)q - x);
+        }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+    }
+    if (lane == 0) err[row] = e * (double)smax;
   }
 }
 
@@ -118,7 +134,9 @@ __global__ void __launch_bounds__(kRunThreads) k_build_runs(const int64_t* __res
                                                             const int32_t* __restrict__ perm,
                                                             const int64_t* __restrict__ rbase,
                                                             uint32_t* __restrict__ runs_f, int32_t* __restrict__ runs_q,
-                                                            uint32_t* __restrict__ batch_nruns, int key_bits) {
+                                                            uint32_t* __restrict__ batch_nruns, int key_bits,
+                                                            const int32_t* __restrict__ gate, int gate_heads) {
+  if (gate && ((*gate > 0) != (gate_heads != 0))) return;  // device-side shape choice (knnjoin_query)
   using BRS = cub::BlockRadixSort<uint32_t, kRunThreads, kRunItems, int32_t>;
   using BScan = cub::BlockScan<int, kRunThreads>;
   __shared__ union {
@@ -237,7 +255,11 @@ __global__ void __launch_bounds__(kRunThreads) k_build_runs(const int64_t* __res
 // ------------------------------------------------------------------------------------ host dispatch
 struct QueryWs {
   size_t sigma_at, inv_at, runs_f_at, runs_q_at, nruns_at, counter_at, state_at, done_at, wkey_at, wkey2_at,
-      perm_at, perm2_at, rlen_at, rbase_at, cub_at, cub_bytes, part_at, part_bytes, prune_at, total;
+      perm_at, perm2_at, rlen_at, rbase_at, cub_at, cub_bytes, part_at, part_bytes, prune_at,
+      // certification + 64-bit fallback (wide.cu): E_r, the final fixed keys, the failing-row list, sigma64,
+      // 1/sigma64, the wide item counter and the tile-group lists of the first kWideCapRows listed rows
+      err_at, keys_at, cert_at, sig64_at, inv64_at, wctr_at, wpart_at, wpart_bytes, done_bytes, total;
+  int32_t wide_G;
 };
 
 // a6 (pruned queries, one row per batch): per run i of a row, prune_suf[i] = the sum of c_j = q_j * maxweight(f_j)
@@ -357,8 +379,25 @@ int64_t split_groups(int64_t n_batches, int64_t ctas) {
   return n_batches < ctas ? (ctas + n_batches - 1) / n_batches : 2;
 }
 
-bool query_ws_layout(int64_t n_r, int64_t nnz_r, int B, int NW, int k, int sms, QueryWs* W) {
-  int64_t n_batches = (n_r + B - 1) / B;
+// shapes: the candidate CTA shapes of the query (one, or the two the device chooses between); every region is
+// sized for the largest need over them
+bool query_ws_layout(int64_t n_r, int64_t nnz_r, const Shape* shapes, int n_shapes, int k, int sms, int64_t n_tiles,
+                     QueryWs* W) {
+  int Bmax = 1, Bmin = 8;
+  size_t part = 0;
+  for (int i = 0; i < n_shapes; ++i) {
+    const int B = shapes[i].B;
+    Bmax = B > Bmax ? B : Bmax;
+    Bmin = B < Bmin ? B : Bmin;
+    // split mode (fewer than kSplitWaves x resident CTAs batches): G tile groups x n_r rows x k keys, with
+    // G <= max(ceil(ctas / n_batches), 2) => G * n_r <= (kSplitWaves * ctas + n_batches) * B
+    const int64_t nb = (n_r + B - 1) / B;
+    const int64_t ctas = (int64_t)sms * ctas_per_sm(shapes[i].NW);
+    const size_t pb = nb < kSplitWaves * ctas ? 8 * (size_t)k * (size_t)((kSplitWaves * ctas + nb) * B) : 0;
+    part = pb > part ? pb : part;
+  }
+  const int64_t n_batches = (n_r + Bmin - 1) / Bmin;
+  const int B = Bmax;
   size_t at = 0;
   W->sigma_at = at;   at = align_up(at + 8 * (size_t)n_r, 256);
   W->inv_at = at;     at = align_up(at + 8 * (size_t)n_r, 256);
@@ -384,13 +423,18 @@ bool query_ws_layout(int64_t n_r, int64_t nnz_r, int B, int NW, int k, int sms, 
   W->rlen_at = at;    at = align_up(at + 8 * (size_t)n_r, 256);
   W->rbase_at = at;   at = align_up(at + 8 * (size_t)n_r, 256);
   W->cub_at = at;     at = align_up(at + W->cub_bytes, 256);
-  // split mode (fewer than kSplitWaves x resident CTAs batches): G tile groups x n_r rows x k keys, with
-  // G <= max(ceil(ctas / n_batches), 2) => G * n_r <= (kSplitWaves * ctas + n_batches) * B
-  const int64_t ctas = (int64_t)sms * ctas_per_sm(NW);
-  W->part_bytes = n_batches < kSplitWaves * ctas
-                      ? 8 * (size_t)k * (size_t)((kSplitWaves * ctas + n_batches) * B) : 0;
+  W->part_bytes = part;
   W->part_at = at;    at = align_up(at + W->part_bytes, 256);
   W->prune_at = at;   at = align_up(at + 8 * (size_t)nnz_r, 256);  // a6 {suffix bound, c} per run (pruned queries)
+  W->err_at = at;     at = align_up(at + 8 * (size_t)n_r, 256);
+  W->keys_at = at;    at = align_up(at + 8 * (size_t)n_r * k, 256);
+  W->cert_at = at;    at = align_up(at + 4 * (size_t)(n_r + 1), 256);
+  W->sig64_at = at;   at = align_up(at + 8 * (size_t)n_r, 256);
+  W->inv64_at = at;   at = align_up(at + 8 * (size_t)n_r, 256);
+  W->wctr_at = at;    at = align_up(at + 16, 256);
+  W->wpart_bytes = wide_part_bytes(k, n_tiles, sms, &W->wide_G);
+  W->done_bytes = 4 * (size_t)n_batches;
+  W->wpart_at = at;   at = align_up(at + W->wpart_bytes, 256);
   W->total = at;
   return true;
 }
@@ -459,13 +503,13 @@ bool check_query_args(const knnjoin_index* idx, const knnjoin_csr* R, int32_t k)
 
 }  // namespace
 
-void launch_row_scale(const knnjoin_csr* R, int32_t d, int32_t smax, double* sigma, double* inv_sigma,
+void launch_row_scale(const knnjoin_csr* R, int32_t d, int32_t smax, double* sigma, double* inv_sigma, double* err,
                       cudaStream_t st) {
   if (R->n_rows <= 0) return;
   int64_t threads = R->n_rows * 32;
   k_row_scale_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
       R->indptr, R->indices, R->dtype == KNNJOIN_FP32 ? (const float*)R->values : nullptr, R->n_rows, d, smax, sigma,
-      inv_sigma);
+      inv_sigma, err);
 }
 
 }  // namespace kj
@@ -476,18 +520,19 @@ KJ_API size_t knnjoin_query_workspace_bytes(const knnjoin_index* idx, const knnj
                                             const knnjoin_query_options* qopt) {
   if (!check_query_args(idx, R, k)) return 0;
   // the auto shape may depend on the index's head count (known on the device): size for both candidates
-  size_t best = 0;
+  Shape shapes[2];
   for (int heads : {0, 1}) {
-    Shape sh;
-    if (!pick_shape(idx->tile, k, qopt ? qopt->batch_rows : 0, qopt ? qopt->cta_warps : 0, heads, &sh)) {
+    if (!pick_shape(idx->tile, k, qopt ? qopt->batch_rows : 0, qopt ? qopt->cta_warps : 0, heads, &shapes[heads])) {
       set_error("no (batch_rows, cta_warps) shape fits shared memory for tile %d, k %d", idx->tile, k);
       return 0;
     }
-    QueryWs W;
-    query_ws_layout(R->n_rows, R->nnz, sh.B, sh.NW, k, device_sms(), &W);
-    if (W.total > best) best = W.total;
   }
-  return best;
+  QueryWs W;
+  if (!query_ws_layout(R->n_rows, R->nnz, shapes, 2, k, device_sms(), idx->n_tiles, &W)) {
+    set_error("workspace sizing failed (CUB temporary storage query)");
+    return 0;
+  }
+  return W.total;
 }
 
 KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr* R, int32_t k,
@@ -496,11 +541,24 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
   if (!check_query_args(idx, R, k)) return KNNJOIN_ERR_ARG;
   if (R->n_rows == 0) return KNNJOIN_OK;  // empty R: nothing to write
   if (!out_keys && (!out_ids || !out_scores)) { set_error("need out_keys or both out_ids and out_scores"); return KNNJOIN_ERR_ARG; }
-  const bool integer = R->dtype != KNNJOIN_FP32;
-  if (integer && (double)idx->d * 127.0 * 127.0 >= 4294967296.0) {
+  const bool s_fp32 = idx->s_dtype == KNNJOIN_FP32;
+  const bool r_fp32 = R->dtype == KNNJOIN_FP32;
+  const int precision = qopt ? qopt->precision : 0;
+  if (precision < 0 || precision > 2) { set_error("precision must be 0 (auto), 1 (32-bit) or 2 (64-bit)"); return KNNJOIN_ERR_ARG; }
+  if (s_fp32 && precision == 1) { set_error("FP32 S is queried at 64-bit fixed point only (precision 0 or 2)"); return KNNJOIN_ERR_UNSUPPORTED; }
+  if (!r_fp32 && !s_fp32 && (double)idx->d * 127.0 * 127.0 >= 4294967296.0) {
     set_error("integer scores may overflow 32 bits for d = %d", idx->d);
     return KNNJOIN_ERR_UNSUPPORTED;
   }
+  if (qopt && (qopt->row_list != nullptr) != (qopt->row_count != nullptr)) {
+    set_error("row_list and row_count go together");
+    return KNNJOIN_ERR_ARG;
+  }
+  if (qopt && !(qopt->tolerance >= 0.0f && qopt->tolerance < 1.0f)) { set_error("tolerance must be in [0, 1)"); return KNNJOIN_ERR_ARG; }
+  const double tol = (qopt && qopt->tolerance > 0.0f) ? (double)qopt->tolerance : kDefaultTolerance;
+  // 64-bit path for the whole query: FP32 S (no 32-bit path), or precision 2 with FP32 R (integer x integer
+  // scores are exact at 32 bits, precision is ignored there)
+  const bool wide_all = s_fp32 || (precision == 2 && r_fp32);
   // a6: effective pruning alpha (0 = not pruned)
   float alpha = 0.0f;
   if (qopt && qopt->prune_alpha != 0.0f && !idx->prune && qopt->prune_alpha > 0.0f) {
@@ -518,22 +576,13 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
     if (qopt->prune_alpha > 0.0f) { set_error("residual (f1) and prune_alpha > 0 (a6) are exclusive"); return KNNJOIN_ERR_ARG; }
     alpha = 0.0f;
   }
-  const bool auto_shape = !qopt || (qopt->batch_rows == 0 && qopt->cta_warps == 0);
-  if (auto_shape && idx->n_head_host < 0) {
-    // first auto-shaped query on this index: read its head count once (4-byte copy; synchronises `stream`)
-    int32_t nh = 0;
-    cudaError_t e0 = cudaMemcpyAsync(&nh, idx->head_feat + kMaxHead, sizeof(nh), cudaMemcpyDeviceToHost,
-                                     (cudaStream_t)stream);
-    if (e0 == cudaSuccess) e0 = cudaStreamSynchronize((cudaStream_t)stream);
-    if (e0 != cudaSuccess) return cuda_fail(e0, "read head count");
-    idx->n_head_host = nh;
-  }
-  Shape sh;
-  if (!pick_shape(idx->tile, k, qopt ? qopt->batch_rows : 0, qopt ? qopt->cta_warps : 0,
-                  idx->n_head_host < 0 ? 1 : (idx->n_head_host > 0 ? 1 : 0), &sh)) {
-    set_error("batch_rows %d / cta_warps %d unsupported for tile %d, k %d", qopt ? qopt->batch_rows : 0,
-              qopt ? qopt->cta_warps : 0, idx->tile, k);
+  if (wide_all && (alpha > 0.0f || residual)) {
+    set_error("64-bit queries (FP32 S or precision 2) do not combine with pruning (a6) or residual (f1) queries");
     return KNNJOIN_ERR_UNSUPPORTED;
+  }
+  if (!wide_all && qopt && qopt->row_list) {
+    set_error("row_list applies to 64-bit queries (FP32 S or precision 2)");
+    return KNNJOIN_ERR_ARG;
   }
   if (qopt && (qopt->tile_begin < 0 || qopt->tile_end < 0 || qopt->tile_begin > idx->n_tiles ||
                qopt->tile_end > idx->n_tiles || (qopt->tile_end > 0 && qopt->tile_begin > qopt->tile_end))) {
@@ -541,28 +590,73 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
               (long long)idx->n_tiles);
     return KNNJOIN_ERR_ARG;
   }
+  const bool auto_shape = !qopt || (qopt->batch_rows == 0 && qopt->cta_warps == 0);
+  // Shapes: an index whose head-feature count may be non-zero (BINARY S with head features enabled) has two
+  // candidate auto shapes, chosen on the DEVICE: both are launched and each gates itself on the index's head
+  // count (the mismatched one returns at entry), so the call never waits for the host to learn the count.
+  const bool may_have_heads = idx->head_max > 0;
+  Shape sh_heads{0, 0}, sh_plain{0, 0};
+  const int req_B = qopt ? qopt->batch_rows : 0, req_NW = qopt ? qopt->cta_warps : 0;
+  if (!pick_shape(idx->tile, k, req_B, req_NW, 0, &sh_plain) ||
+      (may_have_heads && !pick_shape(idx->tile, k, req_B, req_NW, 1, &sh_heads))) {
+    set_error("batch_rows %d / cta_warps %d unsupported for tile %d, k %d", req_B, req_NW, idx->tile, k);
+    return KNNJOIN_ERR_UNSUPPORTED;
+  }
   if ((alpha > 0.0f || residual) && (size_t)((idx->d + 31) / 32) * 4 + smem_bytes(1, idx->tile, k, 4, false) > 200 * 1024) {
     set_error("pruned queries keep a d-bit map in shared memory: d = %d too large", idx->d);
     return KNNJOIN_ERR_UNSUPPORTED;
   }
-  if ((alpha > 0.0f || residual) && !(sh.B == 1 && sh.NW == 4)) {
-    set_error("pruned queries run one-row 4-warp CTAs (batch_rows 1, cta_warps 4); got %d / %d", sh.B, sh.NW);
+  if ((alpha > 0.0f || residual) && !(sh_plain.B == 1 && sh_plain.NW == 4)) {
+    set_error("pruned queries run one-row 4-warp CTAs (batch_rows 1, cta_warps 4); got %d / %d", sh_plain.B, sh_plain.NW);
     return KNNJOIN_ERR_UNSUPPORTED;
   }
-  const int B = sh.B;
+  // the workspace is laid out for the larger of the candidate shapes (only one of them runs)
+  const int sms = device_sms();
   QueryWs W;
-  query_ws_layout(R->n_rows, R->nnz, B, sh.NW, k, device_sms(), &W);
+  {
+    const Shape shapes[2] = {sh_plain, sh_heads};
+    if (!query_ws_layout(R->n_rows, R->nnz, shapes, may_have_heads ? 2 : 1, k, sms, idx->n_tiles, &W)) {
+      set_error("workspace sizing failed (CUB temporary storage query)");
+      return KNNJOIN_ERR_CUDA;
+    }
+  }
   if (!workspace || workspace_bytes < W.total) { set_error("query workspace %zu < %zu bytes", workspace_bytes, W.total); return KNNJOIN_ERR_WORKSPACE; }
   if ((uintptr_t)workspace & 255) { set_error("workspace must be 256-byte aligned"); return KNNJOIN_ERR_ARG; }
-  if (R->n_rows == 0) return KNNJOIN_OK;
   if (!R->indptr || (R->nnz > 0 && !R->indices) || (R->dtype != KNNJOIN_BINARY && R->nnz > 0 && !R->values)) {
     set_error("R pointers are NULL");
     return KNNJOIN_ERR_ARG;
   }
   cudaStream_t st = (cudaStream_t)stream;
   char* wb = (char*)workspace;
+  cudaError_t e;
+  const int64_t t0 = qopt ? qopt->tile_begin : 0;
+  const int64_t t1 = (qopt && qopt->tile_end > 0) ? qopt->tile_end : idx->n_tiles;
+
+  // ------------------------------------------------------------------ 64-bit fixed point for every row
+  if (wide_all) {
+    if (qopt && qopt->ev_begin) cudaEventRecord((cudaEvent_t)qopt->ev_begin, st);
+    e = launch_wide(idx, R, k, t0, t1, qopt ? qopt->row_list : nullptr, qopt ? qopt->row_count : nullptr,
+                    qopt ? qopt->resume_keys : nullptr, qopt ? qopt->theta_in : nullptr, (double*)(wb + W.sig64_at),
+                    (double*)(wb + W.inv64_at), (uint32_t*)(wb + W.wctr_at), (uint64_t*)(wb + W.wpart_at), W.wide_G,
+                    (unsigned long long*)(qopt ? qopt->counters : nullptr), out_keys, out_ids, out_scores, sms, st);
+    if (qopt && qopt->ev_end) cudaEventRecord((cudaEvent_t)qopt->ev_end, st);
+    if (e != cudaSuccess) return cuda_fail(e, "k_accumulate_wide");
+    if (qopt && qopt->uncertified && (e = cudaMemsetAsync(qopt->uncertified, 0, 4, st)) != cudaSuccess)
+      return cuda_fail(e, "memset uncertified");
+    return KNNJOIN_OK;
+  }
+
+  // ------------------------------------------------------------------ 32-bit fixed point (a3-a7)
+  // certification of FP32-R lists (wide.cu): auto mode recomputes failing rows at 64 bits, unless the query is
+  // part of a chained / sharded computation (tile range, resume_keys, theta_in), whose lists only the caller
+  // sees whole (it certifies them with knnjoin_certify)
+  const bool partial = qopt && (qopt->resume_keys || qopt->theta_in || t0 != 0 || t1 != idx->n_tiles);
+  const bool certify = r_fp32 && ((precision == 0 && !partial) || (qopt && qopt->uncertified));
+  const bool fallback = certify && precision == 0 && !partial;
+  uint64_t* keys_dst = out_keys ? out_keys : (certify ? (uint64_t*)(wb + W.keys_at) : nullptr);
   double* sigma = (double*)(wb + W.sigma_at);
   double* inv_sigma = (double*)(wb + W.inv_at);
+  double* err = (double*)(wb + W.err_at);
   uint32_t* runs_f = (uint32_t*)(wb + W.runs_f_at);
   int32_t* runs_q = (int32_t*)(wb + W.runs_q_at);
   uint32_t* nruns = (uint32_t*)(wb + W.nruns_at);
@@ -570,11 +664,9 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
   uint64_t* state_keys = (uint64_t*)(wb + W.state_at);
   uint32_t* pass_done = (uint32_t*)(wb + W.done_at);
   const int32_t smax = idx->s_dtype == KNNJOIN_INT8 ? 127 : 1;
-  const int64_t n_batches = (R->n_rows + B - 1) / B;
-  cudaError_t e;
   if ((e = cudaMemsetAsync(counter, 0, 16, st)) != cudaSuccess) return cuda_fail(e, "memset counter");
-  if ((e = cudaMemsetAsync(pass_done, 0, 4 * (size_t)n_batches, st)) != cudaSuccess) return cuda_fail(e, "memset pass_done");
-  launch_row_scale(R, idx->d, smax, sigma, inv_sigma, st);
+  if ((e = cudaMemsetAsync(pass_done, 0, W.done_bytes, st)) != cudaSuccess) return cuda_fail(e, "memset pass_done");
+  launch_row_scale(R, idx->d, smax, sigma, inv_sigma, certify ? err : nullptr, st);
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_row_scale");
   const int32_t* perm = nullptr;
   const int64_t* rbase = nullptr;
@@ -600,116 +692,145 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
     perm = pm;
     rbase = rb;
   }
-  {
-    int kbits = 3;  // (feature << 3 | row) keys: bits for features < d, plus 3
-    while (kbits < 32 && ((int64_t)1 << (kbits - 3)) <= (int64_t)idx->d) ++kbits;  // invalid keys sort last
-    // block-sort capacity from the mean entries per batch (x1.5 headroom); larger batches use the warp merge
-    const double mean = (double)R->nnz / (double)n_batches * 1.5;
-    if (mean <= kRunThreads * 4)
-      k_build_runs<4><<<(unsigned)n_batches, kRunThreads, 0, st>>>(R->indptr, R->indices, R->values, R->dtype, R->n_rows,
-                                                                   idx->d, B, n_batches, sigma, perm, rbase, runs_f, runs_q, nruns, kbits);
-    else if (mean <= kRunThreads * 8)
-      k_build_runs<8><<<(unsigned)n_batches, kRunThreads, 0, st>>>(R->indptr, R->indices, R->values, R->dtype, R->n_rows,
-                                                                   idx->d, B, n_batches, sigma, perm, rbase, runs_f, runs_q, nruns, kbits);
-    else if (mean <= kRunThreads * 16)
-      k_build_runs<16><<<(unsigned)n_batches, kRunThreads, 0, st>>>(R->indptr, R->indices, R->values, R->dtype, R->n_rows,
-                                                                    idx->d, B, n_batches, sigma, perm, rbase, runs_f, runs_q, nruns, kbits);
-    else
-      k_build_runs<32><<<(unsigned)n_batches, kRunThreads, 0, st>>>(R->indptr, R->indices, R->values, R->dtype, R->n_rows,
-                                                                    idx->d, B, n_batches, sigma, perm, rbase, runs_f, runs_q, nruns, kbits);
-    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_build_runs");
-  }
-  uint2* prune_suf = nullptr;
-  if (alpha > 0.0f) {
-    prune_suf = (uint2*)(wb + W.prune_at);
-    k_prune_prep<<<(unsigned)n_batches, kPruneThreads, 0, st>>>(R->indptr, rbase, runs_f, runs_q, nruns, idx->fmax,
-                                                               prune_suf);
-    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_prune_prep");
-  }
-  QP p;
-  p.off = idx->off;
-  p.ids = idx->ids;
-  p.vals = idx->vals;
-  p.head_slot = idx->head_slot;
-  p.head_feat = idx->head_feat;
-  p.head_cols = idx->head_cols;
-  p.d = idx->d;
-  p.T = idx->tile;
-  p.NT = idx->n_tiles;
-  p.t0 = qopt ? qopt->tile_begin : 0;
-  p.t1 = (qopt && qopt->tile_end > 0) ? qopt->tile_end : idx->n_tiles;
-  p.theta_in = qopt ? qopt->theta_in : nullptr;
-  p.resume = qopt ? qopt->resume_keys : nullptr;
-  p.s_id_base = idx->s_id_base;
-  p.head_smem = idx->n_head_host != 0 ? 1 : 0;  // -1 (unknown) keeps the head tables
-  p.n_r = R->n_rows;
-  p.k = k;
-  p.n_batches = n_batches;
-  p.r_indptr = R->indptr;
-  p.perm = perm;
-  p.rbase = rbase;
-  p.runs_f = runs_f;
-  p.runs_q = runs_q;
-  p.batch_nruns = nruns;
-  p.inv_sigma = inv_sigma;
-  p.batch_counter = counter;
-  {
-    // tiles per pass: a slab of the index small enough to stay in L2 while every batch sweeps it
-    int dev = 0, l2 = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
-    int64_t tpp = qopt ? qopt->tiles_per_pass : 0;
-    if (tpp <= 0) {
-      const double per_tile =
-          (double)(idx->storage_bytes - idx->fwd_bytes) / (double)(idx->n_tiles > 0 ? idx->n_tiles : 1);
-      tpp = (int64_t)((double)(l2 > 0 ? l2 : (96 << 20)) / 3.0 / (per_tile > 1.0 ? per_tile : 1.0));
-      if (tpp < 1) tpp = 1;
-    }
-    const int64_t span = p.t1 - p.t0;
-    if (tpp > span) tpp = span > 0 ? span : 1;
-    // few batches (small R, serving): the tiles are split into G independent groups (split_groups) so that
-    // the G x n_batches items fill the resident CTAs; each group's lists go to part_keys and are merged by
-    // rank
-    p.split = 0;
-    p.part_keys = nullptr;
-    const int64_t ctas = (int64_t)device_sms() * ctas_per_sm(sh.NW);
-    if (!(qopt && qopt->tiles_per_pass) && W.part_bytes && span > 1 && n_batches < kSplitWaves * ctas) {
-      int64_t G = split_groups(n_batches, ctas);
-      if (G > span) G = span;
-      if (G > 1 && (size_t)G * (size_t)R->n_rows * (size_t)k * 8 <= W.part_bytes) {
-        tpp = (span + G - 1) / G;
-        p.split = 1;
-        p.part_keys = (uint64_t*)(wb + W.part_at);
-      }
-    }
-    p.tiles_per_pass = tpp;
-    p.n_passes = span > 0 ? (span + tpp - 1) / tpp : 1;  // an empty range still runs one (tile-less) pass
-  }
-  p.alpha = alpha;
-  p.prune_suf = prune_suf;
-  p.fwd_ptr = idx->fwd_ptr;
-  p.fwd_idx = idx->fwd_idx;
-  p.fwd_val = idx->fwd_val;
-  p.fmax = idx->fmax;
-  p.prune_words = (idx->d + 31) / 32;
-  p.residual = residual ? 1 : 0;
-  p.state_keys = state_keys;
-  p.pass_done = pass_done;
-  p.counters = (unsigned long long*)(qopt ? qopt->counters : nullptr);
-  p.phase = (unsigned long long*)(qopt ? qopt->phase_cycles : nullptr);
-  p.out_keys = out_keys;
-  p.out_ids = out_ids;
-  p.out_scores = out_scores;
-  int dev = 0, sms = 148;
+  int dev = 0, l2 = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (qopt && qopt->ev_begin) cudaEventRecord((cudaEvent_t)qopt->ev_begin, st);
-  e = launch_shape(sh, p, sms, st);
-  if (qopt && qopt->ev_end) cudaEventRecord((cudaEvent_t)qopt->ev_end, st);
-  if (e != cudaSuccess) return cuda_fail(e, "k_accumulate_topk");
-  if (p.split) {  // the tile groups' lists hold disjoint S ids: K4's rank merge gives the one-pass result
-    e = launch_merge_keys(p.part_keys, (int32_t)p.n_passes, R->n_rows, k, inv_sigma, out_keys, out_ids, out_scores, st);
-    if (e != cudaSuccess) return cuda_fail(e, "split merge");
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+  int kbits = 3;  // (feature << 3 | row) keys: bits for features < d, plus 3
+  while (kbits < 32 && ((int64_t)1 << (kbits - 3)) <= (int64_t)idx->d) ++kbits;  // invalid keys sort last
+
+  // one candidate shape: run building (a3) + K3.  gate: the index's head count (device); the launch runs only
+  // when (count > 0) == want_heads.
+  auto run_shape = [&](const Shape& sh, const int32_t* gate, int want_heads, bool first, bool last) -> knnjoin_status {
+    const int B = sh.B;
+    const int64_t n_batches = (R->n_rows + B - 1) / B;
+    const double mean = (double)R->nnz / (double)n_batches * 1.5;
+    // block-sort capacity from the mean entries per batch (x1.5 headroom); larger batches use the warp merge
+    const int items = mean <= kRunThreads * 4 ? 4 : (mean <= kRunThreads * 8 ? 8 : (mean <= kRunThreads * 16 ? 16 : 32));
+    auto runs = [&](auto kern) {
+      kern<<<(unsigned)n_batches, kRunThreads, 0, st>>>(R->indptr, R->indices, R->values, R->dtype, R->n_rows, idx->d, B,
+                                                       n_batches, sigma, perm, rbase, runs_f, runs_q, nruns, kbits,
+                                                       gate, want_heads);
+    };
+    if (items == 4) runs(k_build_runs<4>);
+    else if (items == 8) runs(k_build_runs<8>);
+    else if (items == 16) runs(k_build_runs<16>);
+    else runs(k_build_runs<32>);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_build_runs");
+    uint2* prune_suf = nullptr;
+    if (alpha > 0.0f) {
+      prune_suf = (uint2*)(wb + W.prune_at);
+      k_prune_prep<<<(unsigned)n_batches, kPruneThreads, 0, st>>>(R->indptr, rbase, runs_f, runs_q, nruns, idx->fmax,
+                                                                 prune_suf);
+      if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_prune_prep");
+    }
+    QP p;
+    p.off = idx->off;
+    p.ids = idx->ids;
+    p.vals = idx->vals;
+    p.head_slot = idx->head_slot;
+    p.head_feat = idx->head_feat;
+    p.head_cols = idx->head_cols;
+    p.gate = gate;
+    p.gate_heads = want_heads;
+    p.d = idx->d;
+    p.T = idx->tile;
+    p.NT = idx->n_tiles;
+    p.t0 = t0;
+    p.t1 = t1;
+    p.theta_in = qopt ? qopt->theta_in : nullptr;
+    p.resume = qopt ? qopt->resume_keys : nullptr;
+    p.s_id_base = idx->s_id_base;
+    p.head_smem = want_heads;
+    p.n_r = R->n_rows;
+    p.k = k;
+    p.n_batches = n_batches;
+    p.r_indptr = R->indptr;
+    p.perm = perm;
+    p.rbase = rbase;
+    p.runs_f = runs_f;
+    p.runs_q = runs_q;
+    p.batch_nruns = nruns;
+    p.inv_sigma = inv_sigma;
+    p.batch_counter = counter;
+    {
+      // tiles per pass: a slab of the index small enough to stay in L2 while every batch sweeps it
+      int64_t tpp = qopt ? qopt->tiles_per_pass : 0;
+      if (tpp <= 0) {
+        const double per_tile =
+            (double)(idx->storage_bytes - idx->fwd_bytes) / (double)(idx->n_tiles > 0 ? idx->n_tiles : 1);
+        tpp = (int64_t)((double)(l2 > 0 ? l2 : (96 << 20)) / 3.0 / (per_tile > 1.0 ? per_tile : 1.0));
+        if (tpp < 1) tpp = 1;
+      }
+      const int64_t span = p.t1 - p.t0;
+      if (tpp > span) tpp = span > 0 ? span : 1;
+      // few batches (small R, serving): the tiles are split into G independent groups (split_groups) so that
+      // the G x n_batches items fill the resident CTAs; each group's lists go to part_keys and are merged by
+      // rank
+      p.split = 0;
+      p.part_keys = nullptr;
+      const int64_t ctas = (int64_t)sms * ctas_per_sm(sh.NW);
+      if (!(qopt && qopt->tiles_per_pass) && W.part_bytes && span > 1 && n_batches < kSplitWaves * ctas) {
+        int64_t G = split_groups(n_batches, ctas);
+        if (G > span) G = span;
+        if (G > 1 && (size_t)G * (size_t)R->n_rows * (size_t)k * 8 <= W.part_bytes) {
+          tpp = (span + G - 1) / G;
+          p.split = 1;
+          p.part_keys = (uint64_t*)(wb + W.part_at);
+        }
+      }
+      p.tiles_per_pass = tpp;
+      p.n_passes = span > 0 ? (span + tpp - 1) / tpp : 1;  // an empty range still runs one (tile-less) pass
+    }
+    p.alpha = alpha;
+    p.prune_suf = prune_suf;
+    p.fwd_ptr = idx->fwd_ptr;
+    p.fwd_idx = idx->fwd_idx;
+    p.fwd_val = idx->fwd_val;
+    p.fmax = idx->fmax;
+    p.prune_words = (idx->d + 31) / 32;
+    p.residual = residual ? 1 : 0;
+    p.state_keys = state_keys;
+    p.pass_done = pass_done;
+    p.counters = (unsigned long long*)(qopt ? qopt->counters : nullptr);
+    p.phase = (unsigned long long*)(qopt ? qopt->phase_cycles : nullptr);
+    p.out_keys = keys_dst;
+    p.out_ids = out_ids;
+    p.out_scores = out_scores;
+    if (first && qopt && qopt->ev_begin) cudaEventRecord((cudaEvent_t)qopt->ev_begin, st);
+    e = launch_shape(sh, p, sms, st);
+    if (last && qopt && qopt->ev_end) cudaEventRecord((cudaEvent_t)qopt->ev_end, st);
+    if (e != cudaSuccess) return cuda_fail(e, "k_accumulate_topk");
+    if (p.split) {  // the tile groups' lists hold disjoint S ids: K4's rank merge gives the one-pass result
+      e = launch_merge_keys_gated(p.part_keys, (int32_t)p.n_passes, R->n_rows, k, inv_sigma, gate, want_heads, keys_dst,
+                                  out_ids, out_scores, st);
+      if (e != cudaSuccess) return cuda_fail(e, "split merge");
+    }
+    return KNNJOIN_OK;
+  };
+  knnjoin_status rc;
+  if (!may_have_heads) {
+    if ((rc = run_shape(sh_plain, nullptr, 0, true, true)) != KNNJOIN_OK) return rc;
+  } else if (!auto_shape || (sh_plain.B == sh_heads.B && sh_plain.NW == sh_heads.NW)) {
+    // one shape for both cases (requested explicitly): the instance with the head code handles a zero count
+    if ((rc = run_shape(sh_heads, nullptr, 1, true, true)) != KNNJOIN_OK) return rc;
+  } else {
+    const int32_t* gate = idx->head_feat + kMaxHead;
+    if ((rc = run_shape(sh_heads, gate, 1, true, false)) != KNNJOIN_OK) return rc;
+    if ((rc = run_shape(sh_plain, gate, 0, false, true)) != KNNJOIN_OK) return rc;
+  }
+
+  // ------------------------------------------------------------------ certification + 64-bit fallback
+  if (certify) {
+    int32_t* list = (qopt && qopt->uncertified) ? qopt->uncertified : (int32_t*)(wb + W.cert_at);
+    if ((e = launch_certify(keys_dst, err, R->n_rows, k, tol, list, st)) != cudaSuccess) return cuda_fail(e, "k_certify");
+    if (fallback) {
+      e = launch_wide(idx, R, k, t0, t1, list + 1, list, nullptr, nullptr, (double*)(wb + W.sig64_at),
+                      (double*)(wb + W.inv64_at), (uint32_t*)(wb + W.wctr_at), (uint64_t*)(wb + W.wpart_at), W.wide_G,
+                      nullptr, out_keys, out_ids, out_scores, sms, st);
+      if (e != cudaSuccess) return cuda_fail(e, "k_accumulate_wide (fallback)");
+    }
+  } else if (qopt && qopt->uncertified) {
+    if ((e = cudaMemsetAsync(qopt->uncertified, 0, 4, st)) != cudaSuccess) return cuda_fail(e, "memset uncertified");
   }
   return KNNJOIN_OK;
 }

@@ -17,8 +17,8 @@ from __future__ import annotations
 
 import torch
 
-from ._binding import (FP32, DeviceCSR, knnjoin_build_index, knnjoin_iiib_profile, knnjoin_iiib_split,
-                       knnjoin_iiib_threshold, knnjoin_merge, knnjoin_query)
+from ._binding import (FP32, DeviceCSR, knnjoin_build_index, knnjoin_certify, knnjoin_iiib_profile,
+                       knnjoin_iiib_split, knnjoin_iiib_threshold, knnjoin_merge, knnjoin_query)
 
 
 def iiib_join(R: DeviceCSR, S: DeviceCSR, d: int, k: int, s_block: int, tile: int = 0, counters: bool = True,
@@ -47,9 +47,16 @@ def iiib_join(R: DeviceCSR, S: DeviceCSR, d: int, k: int, s_block: int, tile: in
     if keys is None:  # empty S: every row is padding
         keys = torch.zeros((R.n_rows, k), dtype=torch.int64, device=dev)
     ids, sc, _ = knnjoin_merge(keys.unsqueeze(0).contiguous(), R, d, S.dtype, k, stream=stream)
+    n_unc = 0
+    if R.dtype == FP32:  # certify the final 32-bit lists; failing rows are recomputed at 64 bits
+        lst = knnjoin_certify(keys, R, d, S.dtype, k, stream=stream)
+        n_unc = int(lst[0].item())
+        if n_unc:
+            full = knnjoin_build_index(S, d, tile=tile, stream=stream)
+            knnjoin_query(full, R, k, precision=2, row_list=lst, out=(ids, sc, None), stream=stream)
     if counters:
         c = cnt.cpu().tolist()
         visited, completions = c[0], c[3]
     stats = {"postings_built": built, "postings_iib": int(S.nnz), "postings_visited": visited,
-             "residual_completions": completions, "blocks": blocks}
+             "residual_completions": completions, "blocks": blocks, "uncertified_rows": n_unc}
     return ids, sc, stats

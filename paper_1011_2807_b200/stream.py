@@ -16,7 +16,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from ._binding import BINARY, FP32, INT8, DeviceCSR, knnjoin_build_index, knnjoin_query
+from ._binding import BINARY, FP32, INT8, DeviceCSR, knnjoin_build_index, knnjoin_certify, knnjoin_query
 
 
 class PinnedS:
@@ -43,10 +43,8 @@ class PinnedS:
         return PinnedS(h.indptr, h.indices, h.values, block_rows)
 
 
-def streamed_join(S: PinnedS, R: DeviceCSR, d: int, k: int, tile: int = 0, head_density: float = 0.0,
-                  batch_rows: int = 0, want_keys: bool = False):
-    """Returns (ids int32 [n, k], scores float32 [n, k], keys int64 [n, k] or None) of R against all of S.
-    Device memory: two block slots (CSR) + one block index + R + the [n, k] lists, whatever the size of S."""
+def _sweep(S: PinnedS, R: DeviceCSR, d: int, tile: int, head_density: float, query):
+    """Alg. 1's loop over the S blocks: copy block b+1 under block b's index build + query(idx, last)."""
     dev = R.indptr.device
     compute = torch.cuda.current_stream(dev)
     copy = torch.cuda.Stream(dev)
@@ -75,8 +73,6 @@ def streamed_join(S: PinnedS, R: DeviceCSR, d: int, k: int, tile: int = 0, head_
     for sl in slots:
         sl["free"].record(compute)
     issue_copy(0)
-    keys = None
-    ids = scores = None
     for b in range(nb):
         if b + 1 < nb:
             issue_copy(b + 1)
@@ -88,11 +84,46 @@ def streamed_join(S: PinnedS, R: DeviceCSR, d: int, k: int, tile: int = 0, head_
                         None if S.values is None else sl["values"][:nnz], S.dtype)
         idx = knnjoin_build_index(blk, d, s_id_base=lo, tile=tile, head_density=head_density)
         sl["free"].record(compute)  # the block's CSR is no longer read once its index is built
-        last = b == nb - 1
-        ids, scores, keys = knnjoin_query(idx, R, k, want_keys=(not last) or want_keys, want_ids=last,
-                                          batch_rows=batch_rows, resume_keys=keys)
+        query(idx, b == nb - 1)
     for sl in slots:
         for t in (sl["indptr"], sl["indices"], sl["values"]):
             if t is not None:
                 t.record_stream(copy)
+
+
+def streamed_join(S: PinnedS, R: DeviceCSR, d: int, k: int, tile: int = 0, head_density: float = 0.0,
+                  batch_rows: int = 0, want_keys: bool = False, stats: dict | None = None):
+    """Returns (ids int32 [n, k], scores float32 [n, k], keys int64 [n, k] or None) of R against all of S.
+    Device memory: two block slots (CSR) + one block index + R + the [n, k] lists, whatever the size of S.
+    FP32 R against integer S: the final 32-bit lists are certified (knnjoin_certify) and failing
+    rows are streamed again at 64 bits (their keys are then fp32-keyed; stats['uncertified_rows'])."""
+    narrow = R.dtype == FP32 and S.dtype != FP32
+    st = {"keys": None, "ids": None, "scores": None}
+
+    def q32(idx, last):
+        st["ids"], st["scores"], st["keys"] = knnjoin_query(
+            idx, R, k, want_keys=True, want_ids=last, batch_rows=batch_rows, resume_keys=st["keys"],
+            precision=1 if narrow else 0)
+
+    _sweep(S, R, d, tile, head_density, q32)
+    ids, scores, keys = st["ids"], st["scores"], st["keys"]
+    n_unc = 0
+    if narrow:
+        lst = knnjoin_certify(keys, R, d, S.dtype, k)
+        n_unc = int(lst[0].item())
+        if n_unc:
+            wk = [torch.zeros_like(keys), torch.zeros_like(keys)]
+            step = {"b": 0}
+
+            def q64(idx, last):
+                b = step["b"]
+                src = wk[(b + 1) % 2] if b > 0 else None
+                dst = wk[b % 2]
+                out = (ids, scores, keys) if last else (None, None, dst)
+                knnjoin_query(idx, R, k, precision=2, row_list=lst, resume_keys=src, out=out)
+                step["b"] = b + 1
+
+            _sweep(S, R, d, tile, head_density, q64)
+    if stats is not None:
+        stats["uncertified_rows"] = n_unc
     return ids, scores, keys if want_keys else None

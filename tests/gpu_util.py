@@ -9,7 +9,8 @@ TOL = 1e-5  # BASELINE.json north_star: fp32 scores within 1e-5 relative
 
 
 def gpu_join(R, S, k, d=None, tile=0, batch_rows=0, s_id_base=0, want_keys=False, counters=None, head_density=0.0,
-             head_max=0, cta_warps=0, tiles_per_pass=0, row_order=0, prune=0, alpha=0.0, prune_alpha=0.0):
+             head_max=0, cta_warps=0, tiles_per_pass=0, row_order=0, prune=0, alpha=0.0, prune_alpha=0.0,
+             precision=0, uncertified=None):
     import paper_1011_2807_b200 as kj
     d = d or R.d
     dS = kj.DeviceCSR.from_host(S)
@@ -18,7 +19,7 @@ def gpu_join(R, S, k, d=None, tile=0, batch_rows=0, s_id_base=0, want_keys=False
                                  prune=prune, alpha=alpha)
     ids, sc, keys = kj.knnjoin_query(idx, dR, k, want_keys=want_keys, batch_rows=batch_rows, counters=counters,
                                      cta_warps=cta_warps, tiles_per_pass=tiles_per_pass, row_order=row_order,
-                                     prune_alpha=prune_alpha)
+                                     prune_alpha=prune_alpha, precision=precision, uncertified=uncertified)
     torch.cuda.synchronize()
     out = (ids.cpu().numpy().astype(np.int64), sc.cpu().numpy().astype(np.float64))
     if want_keys:

@@ -46,10 +46,15 @@ def test_index_bytes_host_only():
     at = al(at + 4 * 10_000)    # head_slot
     at = al(at + 4 * 33)        # head_feat + n_head
     at = al(at + 4 * nt * 8192)  # head_cols
-    assert n == al(at + 16 * cap)
+    at = al(at + 16 * cap)       # ids
+    assert n == al(at + 4)       # wmax
+    # FP32 S: 8 fp32 weights per 16-byte unit of ids
+    Sf = b._CSR(100_000, 4_000_000, 0, 0, 0, b.FP32)
+    nf = L.knnjoin_index_bytes(ctypes.byref(Sf), 10_000, ctypes.byref(opt))
+    assert nf == al(at + 32 * cap) + 256
 
 
-@pytest.mark.parametrize("d,tile,dtype,msg", [(0, 8192, 0, "d must be"), (100, 1000, 0, "tile"), (100, 8192, 2, "dtype")])
+@pytest.mark.parametrize("d,tile,dtype,msg", [(0, 8192, 0, "d must be"), (100, 1000, 0, "tile"), (100, 8192, 7, "dtype")])
 def test_build_argument_errors(d, tile, dtype, msg):
     import paper_1011_2807_b200._binding as b
     L = b._lib
@@ -75,6 +80,10 @@ def test_prune_index_bytes_and_argument_errors():
                      (b._Options(8192, 0, 0.5, 0.0, 0), "alpha")):
         assert L.knnjoin_index_bytes(ctypes.byref(S), 100, ctypes.byref(opt)) == 0
         assert msg in b.knnjoin_last_error()
+    # FP32 S has no 32-bit path: pruned (a6) / residual (f1) indexes need BINARY or INT8 S
+    Sf = b._CSR(10, 20, 0, 0, 0, b.FP32)
+    assert L.knnjoin_index_bytes(ctypes.byref(Sf), 100, ctypes.byref(b._Options(8192, 1, 0.5, 0.0, 0))) == 0
+    assert "FP32 S" in b.knnjoin_last_error()
 
 
 def test_ctypes_structs_match_the_c_header(tmp_path):
@@ -86,7 +95,7 @@ def test_ctypes_structs_match_the_c_header(tmp_path):
     if cc is None:
         pytest.skip("no C compiler")
     structs = {"knnjoin_csr": b._CSR, "knnjoin_options": b._Options, "knnjoin_query_options": b._QueryOptions,
-               "knnjoin_index_info": b._IndexInfo}
+               "knnjoin_index_info": b._IndexInfo, "knnjoin_merge_options": b._MergeOptions}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "knnjoin.h"', "int main(void) {"]
     for cname, cls in structs.items():
         lines.append(f'  printf("{cname} %zu\\n", sizeof({cname}));')

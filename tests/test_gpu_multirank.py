@@ -28,7 +28,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, name, n_r, n_s, theta_tiles, q):
+def _worker(rank, world, port, name, n_r, n_s, theta_tiles, q, hdr=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     sys.path.insert(0, ROOT)
@@ -38,13 +38,22 @@ def _worker(rank, world, port, name, n_r, n_s, theta_tiles, q):
         import paper_1011_2807_b200 as kj
         from paper_1011_2807_b200 import dist as kdist
         c = gen.CONFIGS[name].scaled(n_r, n_s)
-        R = gen.generate(c, "R")
-        lo, hi = kdist.shard_bounds(n_s, world, rank)
-        S_shard = gen.generate(c, "S", lo, hi - lo)
-        ids, sc = kdist.dist_query(kj.DeviceCSR.from_host(S_shard), lo, kj.DeviceCSR.from_host(R), c.d, c.k,
-                                   tile=2048, theta_tiles=theta_tiles)
+        if hdr:
+            from tests.test_gpu_precision import dynamic_range_case
+            R, S = dynamic_range_case(n_r, n_s)
+            lo, hi = kdist.shard_bounds(n_s, world, rank)
+            S_shard = S.take_rows(np.arange(lo, hi))
+            d, k = R.d, 10
+        else:
+            R = gen.generate(c, "R")
+            lo, hi = kdist.shard_bounds(n_s, world, rank)
+            S_shard = gen.generate(c, "S", lo, hi - lo)
+            d, k = c.d, c.k
+        st = {}
+        ids, sc = kdist.dist_query(kj.DeviceCSR.from_host(S_shard), lo, kj.DeviceCSR.from_host(R), d, k,
+                                   tile=2048, theta_tiles=theta_tiles, stats=st)
         torch.cuda.synchronize()
-        q.put((rank, ids.cpu().numpy(), sc.cpu().numpy()))
+        q.put((rank, ids.cpu().numpy(), sc.cpu().numpy(), st.get("uncertified_rows", 0)))
     finally:
         dist.destroy_process_group()
 
@@ -69,7 +78,39 @@ def test_dist_query_two_ranks_one_gpu(name, theta_tiles):
     c = gen.CONFIGS[name].scaled(n_r, n_s)
     R, S = gen.generate(c, "R"), gen.generate(c, "S")
     ref_ids, ref_sc = gpu_join(R, S, c.k, tile=2048)
-    for _, ids, sc in res:
+    for _, ids, sc, _ in res:
+        np.testing.assert_array_equal(ids, ref_ids)
+        np.testing.assert_array_equal(sc, ref_sc.astype(np.float32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("theta_tiles", [0, 2])
+def test_dist_query_certified_fallback_two_ranks(theta_tiles):
+    """High-dynamic-range FP32 rows through dist.dist_query on 2 ranks: the merged 32-bit lists of some rows fail
+    certification on every rank alike, those rows are recomputed at 64 bits on both shards and merged again; the
+    result meets the 1e-5 rule against the oracle and equals the one-index (auto) result bit for bit (binary S:
+    the same 64-bit scale on both shards)."""
+    import oracle
+    from tests.gpu_util import assert_parity
+    from tests.test_gpu_precision import dynamic_range_case
+    n_r, n_s, world = 40, 12000, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, "C2", n_r, n_s, theta_tiles, q, True))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    R, S = dynamic_range_case(n_r, n_s)
+    ref_ids, ref_sc = gpu_join(R, S, 10, tile=2048)
+    o_ids, o_sc = oracle.knn(R, S, 10, threads=8)
+    for _, ids, sc, n_unc in res:
+        assert n_unc > 0
+        assert_parity(R, S, ids.astype(np.int64), sc.astype(np.float64), o_ids, o_sc)
         np.testing.assert_array_equal(ids, ref_ids)
         np.testing.assert_array_equal(sc, ref_sc.astype(np.float32))
 
@@ -88,5 +129,6 @@ def test_bench_two_ranks_gloo_one_gpu(extra):
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, r.stdout[-2000:]
     j = json.loads(lines[0])
-    assert j["n_gpus"] == 2 and j["value"] > 0 and j["config"]["S_rows_total"] == 2 * j["config"]["S_rows_per_gpu"]
+    assert j["n_gpus"] == 2 and j["value"] > 0 and j["scaling"] == "strong"
+    assert j["config"]["S_rows_total"] == 10_000 and j["config"]["S_rows_this_rank"] == 5_000  # C1's S, split
     assert j["e2e"]["value"] > 0

@@ -290,6 +290,18 @@ def test_full_size_sampled_rows(name, n_sample):
     assert_parity(R.take_rows(rows), S, g_ids[rows], g_sc[rows], o_ids, o_sc, rows=None)
 
 
+@pytest.mark.slow
+def test_full_size_C2_every_row():
+    """C2 (BASELINE.json configs[1]) at full size, in the bench's launch configuration: EVERY one of the 10,000
+    rows against all 100,000 rows of S checked by the oracle (1e9 pairs; rows split over the host's threads)."""
+    import os
+    c = gen.CONFIGS["C2"]
+    R, S = gen.generate(c, "R"), gen.generate(c, "S")
+    g_ids, g_sc = gpu_join(R, S, c.k)
+    o_ids, o_sc = oracle.knn(R, S, c.k, threads=max(1, len(os.sched_getaffinity(0))))
+    assert_parity(R, S, g_ids, g_sc, o_ids, o_sc)
+
+
 @pytest.mark.parametrize("name,tpp", [("C2", 1), ("C2", 3), ("C3", 2), ("C5", 1)])
 def test_tile_passes_identical(name, tpp):
     """Pass-major schedule (top-k state carried between passes in the workspace) == single pass, bit for bit."""

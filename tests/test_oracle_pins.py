@@ -10,7 +10,7 @@ import pytest
 
 import oracle
 from oracle import paper_algs as pa
-from tests.util import csr_from_rows, random_csr, scipy_topk, stable_seed
+from tests.util import csr_from_rows, random_csr, scipy_topk, stable_seed, to_scipy
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
@@ -114,6 +114,35 @@ def test_knn_edge_cases():
     assert (ids == -1).all() and (sc == 0).all()
     ids, sc = oracle.knn(R, S, 2, rows=[2, 0])
     assert ids.tolist() == [[-1, -1], [1, 0]]
+
+
+@pytest.mark.parametrize("dtype_r,dtype_s", [("binary", "binary"), ("int8", "int8"), ("fp32", "binary"),
+                                             ("fp32", "int8"), ("fp32", "fp32"), ("int8", "fp32")])
+def test_pair_scores_match_scipy_matrix(dtype_r, dtype_s):
+    """oracle_pair_scores (the x(.) of every fp32 parity check, reading c15) == the entries
+    M[r, s] of the textbook SpGEMM M = R @ S.T (Eq. 1) for arbitrary (r, s) pairs, in any order
+    and with repeats; s < 0 (padding) gives 0.  Integer inputs exactly; fp32 within fp64 summation rounding."""
+    rng = np.random.default_rng(stable_seed("pairs", dtype_r, dtype_s))
+    d = 70
+    R = random_csr(rng, 30, d, 0, 25, dtype_r, vmax=9)
+    S = random_csr(rng, 90, d, 0, 25, dtype_s, vmax=9)
+    M = (to_scipy(R) @ to_scipy(S).T).toarray()
+    rr = rng.integers(0, R.n_rows, size=2000)
+    ss = rng.integers(-1, S.n_rows, size=2000)  # -1: padding position
+    rr[:30], ss[:30] = np.arange(30), np.arange(30)  # the diagonal and repeats
+    got = oracle.pair_scores(R, S, rr, ss)
+    want = np.where(ss >= 0, M[rr, np.maximum(ss, 0)], 0.0)
+    if "fp32" in (dtype_r, dtype_s):
+        np.testing.assert_allclose(got, want, rtol=1e-13, atol=0)
+    else:
+        np.testing.assert_array_equal(got, want)
+    assert np.all(got[ss < 0] == 0.0)
+    # the pairs of a GPU list carry global ids: assert_parity maps them back with s_id_base; the same oracle
+    # top-k with s_id_base=1000 must give scores equal to pair_scores of (id - 1000)
+    ids, sc = oracle.knn(R, S, 5, s_id_base=1000)
+    loc = np.where(ids >= 0, ids - 1000, -1)
+    np.testing.assert_array_equal(oracle.pair_scores(R, S, np.repeat(np.arange(R.n_rows), 5), loc.ravel()),
+                                  sc.ravel())
 
 
 def test_oracle_threads_split_rows_only():
@@ -262,3 +291,31 @@ def test_iiib_split_soundness_and_fewer_postings():
             idx = sorted((dd, w) for dd, lst in inv.items() for sj, w in lst if sj == si)
             assert sorted(idx + res[si]) == sorted(s)
         assert c.postings_built <= sum(len(s) for _, s in Bs)
+
+
+@pytest.mark.parametrize("dtype_r,dtype_s", [("binary", "binary"), ("int8", "int8"), ("fp32", "binary"),
+                                             ("fp32", "int8"), ("fp32", "fp32")])
+@pytest.mark.parametrize("k", [1, 4, 30])
+def test_cpu_iib_equals_oracle(dtype_r, dtype_s, k):
+    """The host IIB baseline (oracle/iib.c, Alg. 3) returns the oracle's lists: bit for bit on integer inputs
+    (ids included, tie-heavy), within fp64 summation rounding on fp32 ones; its posting count is Eq. 4's second
+    term sum_d n_R(d) n_S(d)."""
+    rng = np.random.default_rng(stable_seed("iib", dtype_r, dtype_s, k))
+    d = 60
+    R = random_csr(rng, 30, d, 0, 20, dtype_r, vmax=3)
+    S = random_csr(rng, 300, d, 0, 20, dtype_s, vmax=3)
+    ids, sc, info = oracle.iib_knn(R, S, k, threads=3)
+    o_ids, o_sc = oracle.knn(R, S, k)
+    nR = np.bincount(R.indices, minlength=d).astype(np.int64)
+    nS = np.bincount(S.indices, minlength=d).astype(np.int64)
+    assert info["visits"] == int((nR * nS).sum())
+    if "fp32" in (dtype_r, dtype_s):
+        np.testing.assert_allclose(sc, o_sc, rtol=1e-12, atol=0)
+        M = (to_scipy(R) @ to_scipy(S).T).toarray()
+        for i in range(R.n_rows):
+            for t in range(k):
+                if ids[i, t] != o_ids[i, t]:
+                    assert abs(M[i, ids[i, t]] - M[i, o_ids[i, t]]) <= 1e-12 * M[i, o_ids[i, t]]
+    else:
+        np.testing.assert_array_equal(ids, o_ids)
+        np.testing.assert_array_equal(sc, o_sc)
