@@ -147,8 +147,9 @@ typedef struct {
  *              meets the tolerance rule of DESIGN.md reading c15 when E_r (2 + tol) <= (tol - 2^-23) y_min -- and
  *              the rows that fail are recomputed at 64-bit fixed point (wide.cu), which holds the rule at any
  *              dynamic range of practical inputs (weights spanning many decades).  Auto skips the
- *              recomputation in a partial query (tile range, resume_keys or theta_in): the caller certifies the
- *              complete lists with knnjoin_certify.  1: 32-bit only (with `uncertified`, the failing rows are
+ *              recomputation in a partial query (tile range, resume_keys, theta_in, or a residual query): the
+ *              caller certifies the complete lists with knnjoin_certify.  A query whose keys a later query resumes
+ *              must use precision 1, so that every resumed list keeps the 32-bit key encoding.  1: 32-bit only (with `uncertified`, the failing rows are
  *              reported, not recomputed).  2: 64-bit for every row.  Integer R with integer S is exact at 32 bits
  *              (precision is ignored); FP32 S always runs at 64 bits (1 -> KNNJOIN_ERR_UNSUPPORTED).
  *              KEY ENCODING: 32-bit results key the fixed-point score (score field = the row's fixed-point sum,

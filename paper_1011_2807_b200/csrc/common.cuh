@@ -56,9 +56,11 @@ int ks_for_k(int32_t k);
 cudaError_t launch_merge_keys(const uint64_t* keys, int32_t P, int64_t n, int32_t k, const double* inv_sigma,
                               uint64_t* out_keys, int32_t* out_ids, float* out_scores, cudaStream_t st);
 // float_keys: scores are fp32 bits (wide queries); row_list/row_count: position i -> output row row_list[i]
-cudaError_t launch_merge_keys_ex(const uint64_t* keys, int32_t P, int64_t n, int32_t k, const double* inv_sigma,
-                                 int float_keys, const int32_t* row_list, const int32_t* row_count, int keys_by_row,
-                                 uint64_t* out_keys, int32_t* out_ids, float* out_scores, cudaStream_t st);
+// n: slab stride in rows; limit: list positions merged (<= n)
+cudaError_t launch_merge_keys_ex(const uint64_t* keys, int32_t P, int64_t n, int64_t limit, int32_t k,
+                                 const double* inv_sigma, int float_keys, const int32_t* row_list,
+                                 const int32_t* row_count, int keys_by_row, uint64_t* out_keys, int32_t* out_ids,
+                                 float* out_scores, cudaStream_t st);
 // 64-bit fixed-point queries (wide.cu)
 size_t wide_part_bytes(int32_t k, int64_t n_tiles, int sms, int32_t* G_out);
 cudaError_t launch_wide(const knnjoin_index* idx, const knnjoin_csr* R, int32_t k, int64_t t0, int64_t t1,

@@ -39,16 +39,17 @@ namespace {
 // larger keys in the other P-1 lists (binary searches); positions past the row's positive keys are padding.
 // float_keys: the score field is fp32 bits of the score (64-bit fixed-point queries, wide.cu), else a 32-bit
 // fixed-point sum decoded with inv_sigma.  row_list / row_count: list position i holds output row row_list[i]
-// (only the first *row_count positions are merged); nullptr: position i is row i.  keys_by_row: the lists of
+// (only the first *row_count positions are merged); nullptr: position i is row i.  n: slab stride (rows per
+// slab); limit: positions merged (<= n).  keys_by_row: the lists of
 // listed row r sit at slab position r (a [P][n][k] gather of whole-R outputs), else at list position i.
-__global__ void k_merge(const uint64_t* __restrict__ keys, int32_t P, int64_t n, int32_t k,
+__global__ void k_merge(const uint64_t* __restrict__ keys, int32_t P, int64_t n, int64_t limit, int32_t k,
                         const double* __restrict__ inv_sigma, int float_keys, const int32_t* __restrict__ row_list,
                         const int32_t* __restrict__ row_count, int keys_by_row, const int32_t* __restrict__ gate,
                         int gate_heads, uint64_t* out_keys, int32_t* out_ids, float* out_scores) {
   if (gate && ((*gate > 0) != (gate_heads != 0))) return;
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (i >= n || (row_count && i >= (int64_t)*row_count)) return;
+  if (i >= limit || (row_count && i >= (int64_t)*row_count)) return;
   const int64_t r = row_list ? (int64_t)row_list[i] : i;
   const int64_t at = keys_by_row ? r : i;
   auto list = [&](int pr) { return keys + ((size_t)pr * n + at) * k; };
@@ -89,12 +90,13 @@ __global__ void k_merge(const uint64_t* __restrict__ keys, int32_t P, int64_t n,
 
 }  // namespace
 
-cudaError_t launch_merge_keys_ex(const uint64_t* keys, int32_t P, int64_t n, int32_t k, const double* inv_sigma,
-                                 int float_keys, const int32_t* row_list, const int32_t* row_count, int keys_by_row,
-                                 uint64_t* out_keys, int32_t* out_ids, float* out_scores, cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
-  const int64_t threads = n * 32;
-  k_merge<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(keys, P, n, k, inv_sigma, float_keys, row_list, row_count,
+cudaError_t launch_merge_keys_ex(const uint64_t* keys, int32_t P, int64_t n, int64_t limit, int32_t k,
+                                 const double* inv_sigma, int float_keys, const int32_t* row_list,
+                                 const int32_t* row_count, int keys_by_row, uint64_t* out_keys, int32_t* out_ids,
+                                 float* out_scores, cudaStream_t st) {
+  if (limit <= 0) return cudaSuccess;
+  const int64_t threads = limit * 32;
+  k_merge<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(keys, P, n, limit, k, inv_sigma, float_keys, row_list, row_count,
                                                              keys_by_row, nullptr, 0, out_keys, out_ids, out_scores);
   return cudaGetLastError();
 }
@@ -104,14 +106,14 @@ cudaError_t launch_merge_keys_gated(const uint64_t* keys, int32_t P, int64_t n, 
                                     float* out_scores, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const int64_t threads = n * 32;
-  k_merge<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(keys, P, n, k, inv_sigma, 0, nullptr, nullptr, 0, gate,
+  k_merge<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(keys, P, n, n, k, inv_sigma, 0, nullptr, nullptr, 0, gate,
                                                              gate_heads, out_keys, out_ids, out_scores);
   return cudaGetLastError();
 }
 
 cudaError_t launch_merge_keys(const uint64_t* keys, int32_t P, int64_t n, int32_t k, const double* inv_sigma,
                               uint64_t* out_keys, int32_t* out_ids, float* out_scores, cudaStream_t st) {
-  return launch_merge_keys_ex(keys, P, n, k, inv_sigma, 0, nullptr, nullptr, 0, out_keys, out_ids, out_scores, st);
+  return launch_merge_keys_ex(keys, P, n, n, k, inv_sigma, 0, nullptr, nullptr, 0, out_keys, out_ids, out_scores, st);
 }
 
 namespace {
@@ -177,7 +179,7 @@ KJ_API knnjoin_status knnjoin_merge(const uint64_t* keys, int32_t P, const knnjo
   if (!float_keys) launch_row_scale(R, d, s_dtype == KNNJOIN_INT8 ? 127 : 1, nullptr, inv, nullptr, st);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "row scale");
-  if ((e = launch_merge_keys_ex(keys, P, R->n_rows, k, inv, float_keys, mopt ? mopt->row_list : nullptr,
+  if ((e = launch_merge_keys_ex(keys, P, R->n_rows, R->n_rows, k, inv, float_keys, mopt ? mopt->row_list : nullptr,
                                 mopt ? mopt->row_count : nullptr, 1, out_keys, out_ids, out_scores, st)) != cudaSuccess)
     return cuda_fail(e, "k_merge");
   return KNNJOIN_OK;

@@ -650,7 +650,9 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
   // certification of FP32-R lists (wide.cu): auto mode recomputes failing rows at 64 bits, unless the query is
   // part of a chained / sharded computation (tile range, resume_keys, theta_in), whose lists only the caller
   // sees whole (it certifies them with knnjoin_certify)
-  const bool partial = qopt && (qopt->resume_keys || qopt->theta_in || t0 != 0 || t1 != idx->n_tiles);
+  // (a residual query's index holds only the indexed parts s'' of S: a 64-bit re-run over it would miss dot(r, s'),
+  // so f1's caller certifies and recomputes at the end as well)
+  const bool partial = qopt && (qopt->resume_keys || qopt->theta_in || t0 != 0 || t1 != idx->n_tiles || residual);
   const bool certify = r_fp32 && ((precision == 0 && !partial) || (qopt && qopt->uncertified));
   const bool fallback = certify && precision == 0 && !partial;
   uint64_t* keys_dst = out_keys ? out_keys : (certify ? (uint64_t*)(wb + W.keys_at) : nullptr);

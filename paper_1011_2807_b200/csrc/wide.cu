@@ -440,9 +440,10 @@ cudaError_t launch_wide(const knnjoin_index* idx, const knnjoin_csr* R, int32_t 
   e = KS == 1 ? go(k_accumulate_wide<1>) : (KS == 4 ? go(k_accumulate_wide<4>) : go(k_accumulate_wide<8>));
   if (e != cudaSuccess) return e;
   if (G > 1) {
-    const int64_t n = row_list ? kWideCapRows : (R->n_rows < kWideCapRows ? R->n_rows : kWideCapRows);
-    return launch_merge_keys_ex(part_keys, G, n, k, nullptr, 1, row_list, row_count, 0, out_keys, out_ids, out_scores,
-                                st);
+    // the part lists have a stride of kWideCapRows rows; positions >= min(count, kWideCapRows) are not grouped
+    const int64_t limit = row_list ? kWideCapRows : (R->n_rows < kWideCapRows ? R->n_rows : kWideCapRows);
+    return launch_merge_keys_ex(part_keys, G, kWideCapRows, limit, k, nullptr, 1, row_list, row_count, 0, out_keys,
+                                out_ids, out_scores, st);
   }
   return cudaSuccess;
 }

@@ -42,7 +42,7 @@ def iiib_join(R: DeviceCSR, S: DeviceCSR, d: int, k: int, s_block: int, tile: in
         built += s_idx.nnz
         idx = knnjoin_build_index(s_idx, d, s_id_base=lo, tile=tile, prune=1, forward=s_res, stream=stream)
         _, _, keys = knnjoin_query(idx, R, k, want_keys=True, want_ids=False, resume_keys=keys, residual=1,
-                                   counters=cnt, stream=stream)
+                                   counters=cnt, stream=stream, precision=1)
         blocks += 1
     if keys is None:  # empty S: every row is padding
         keys = torch.zeros((R.n_rows, k), dtype=torch.int64, device=dev)

@@ -68,7 +68,7 @@ def test_dynamic_range_auto_meets_tolerance(s_dtype):
     flagged = set(u[1:1 + u[0]].tolist())
     assert len(flagged) > 0
     n_ids, n_sc = gpu_join(R, S, k, tile=2048, precision=1)
-    keep = np.array([i for i in range(R.n_rows) if i not in flagged])
+    keep = np.array([i for i in range(R.n_rows) if i not in flagged], dtype=np.int64)
     np.testing.assert_array_equal(ids[keep], n_ids[keep])
     np.testing.assert_array_equal(sc[keep], n_sc[keep])
 
@@ -85,7 +85,7 @@ def test_dynamic_range_certification_is_sound(s_dtype):
     u = unc.cpu().numpy()
     flagged = set(u[1:1 + u[0]].tolist())
     assert flagged
-    ok_rows = np.array([i for i in range(R.n_rows) if i not in flagged])
+    ok_rows = np.array([i for i in range(R.n_rows) if i not in flagged], dtype=np.int64)
     if len(ok_rows):
         assert_parity(R.take_rows(ok_rows), S, ids[ok_rows], sc[ok_rows], o_ids[ok_rows], o_sc[ok_rows],
                       rows=None)
@@ -296,3 +296,28 @@ def test_streamed_and_iiib_joins_certified():
     torch.cuda.synchronize()
     assert stats["uncertified_rows"] > 0
     assert_parity(R, S, ids.cpu().numpy().astype(np.int64), sc.cpu().numpy().astype(np.float64), o_ids, o_sc)
+
+
+@pytest.mark.parametrize("dts", ["int8", "binary", "fp32"])
+@pytest.mark.parametrize("k,n_r", [(1, 24), (10, 24), (10, 100)])
+def test_wide_random_against_oracle(dts, k, n_r):
+    """The 64-bit path alone (precision 2, FP32 R) on small random multi-tile inputs, all rows and a row list:
+    fewer and more listed rows than the 64 that are split into tile groups."""
+    import paper_1011_2807_b200 as kj
+    rng = np.random.default_rng(stable_seed("wide", dts, k, n_r))
+    d = 200
+    R = random_csr(rng, n_r, d, 0, 30, "fp32")
+    S = random_csr(rng, 6000, d, 0, 25, dts, vmax=4)
+    o_ids, o_sc = _oracle(R, S, k)
+    ids, sc = gpu_join(R, S, k, tile=2048, precision=2)
+    assert_parity(R, S, ids, sc, o_ids, o_sc)
+    rows = np.arange(1, n_r, 2, dtype=np.int32)
+    lst = torch.from_numpy(np.concatenate([[len(rows)], rows]).astype(np.int32)).cuda()
+    dR, dS = kj.DeviceCSR.from_host(R), kj.DeviceCSR.from_host(S)
+    idx = kj.knnjoin_build_index(dS, d, tile=2048)
+    g_ids = torch.full((n_r, k), -7, dtype=torch.int32, device="cuda")
+    g_sc = torch.zeros((n_r, k), dtype=torch.float32, device="cuda")
+    kj.knnjoin_query(idx, dR, k, precision=2, row_list=lst, out=(g_ids, g_sc, None))
+    torch.cuda.synchronize()
+    g_ids, g_sc = g_ids.cpu().numpy().astype(np.int64), g_sc.cpu().numpy().astype(np.float64)
+    assert_parity(R.take_rows(rows), S, g_ids[rows], g_sc[rows], o_ids[rows], o_sc[rows], rows=None)
