@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--tiles-per-pass", type=int, default=0)
     ap.add_argument("--row-order", type=int, default=0, help="0 work-sorted (a3), 1 input order")
     ap.add_argument("--head-density", type=float, default=0.0, help="0 auto (1/8), <0 no head features")
-    ap.add_argument("--head-max", type=int, default=0, help="0 auto (64)")
+    ap.add_argument("--head-max", type=int, default=0, help="0 auto (32)")
     ap.add_argument("--theta-tiles", type=int, default=0,
                     help="N>1: f2 cross-rank threshold every this many S tiles (0 = off)")
     ap.add_argument("--prune-alpha", type=float, default=0.0,

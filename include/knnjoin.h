@@ -60,7 +60,8 @@ typedef struct {
 } knnjoin_csr;
 
 /* Build options.  tile: S ids per tile (the S-block of Alg. 1 mapped to a shared-memory score array);
- * 0 = default 8192; must be a multiple of 2048 and <= 32768.
+ * 0 = default 8192; must be a multiple of 2048 and <= 14336 (posting ids are stored as 16-bit byte offsets of
+ * their score column, 4 * local id).
  * prune / alpha: prune = 1 builds the index for the threshold-pruned query mode (the
  *   r-side form of IIIB's threshold refinement, PAPER.md:161-173 and Alg. 4): the storage
  *   additionally keeps S's forward rows (indptr, features, int8 weights) and, for INT8 S, the largest weight
@@ -214,8 +215,8 @@ size_t knnjoin_build_workspace_bytes(const knnjoin_csr* S, int32_t d, const knnj
 /* Build the tiled inverted index of S (BINARY, INT8 or FP32 weights) into `index_storage` (>= knnjoin_index_bytes bytes, 256-byte
  * aligned) using `workspace` (>= knnjoin_build_workspace_bytes bytes).  Layout:
  * for tile t (S ids [t*tile, (t+1)*tile)) and feature f, the postings of I_f restricted to the tile are a
- * contiguous, 16-byte aligned slice of local ids (+ uint8 values for INT8 S), padded with dummy ids
- * tile + (0..31); inside each full 256-posting block postings are ordered by shared-memory bank, the last
+ * contiguous, 16-byte aligned slice of local ids stored as byte offsets 4 * (s - tile base) (+ uint8 / fp32 values
+ * for INT8 / FP32 S), padded with dummy ids 4 * (tile + (0..31)); inside each full 256-posting block postings are ordered by shared-memory bank, the last
  * partial block is transposed so a warp's lanes touch consecutive ids; head features (see head_density)
  * are stored as one 32-bit word per S row instead of id lists.
  * s_id_base: global id of S row 0 (ids returned by queries are s_id_base + local row).

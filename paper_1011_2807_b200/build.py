@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libknnjoin.so")
 BUILD = os.path.join(HERE, "build")
-SOURCES = ["index_build.cu", "query.cu", "merge.cu", "accumulate_ks1.cu", "accumulate_ks4.cu", "accumulate_ks8.cu", "iiib.cu", "wide.cu"]
+SOURCES = ["index_build.cu", "query.cu", "merge.cu", "accumulate_ks1.cu", "accumulate_ks4.cu", "accumulate_ks8.cu", "iiib.cu", "wide.cu", "accumulate_short.cu"]
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
@@ -55,4 +55,11 @@ def build(force: bool = False, verbose: bool = True) -> str:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv)
+    # --src DIR --out FILE: build a variant library from another source tree (A/B experiments, tools/ab.py)
+    if "--src" in sys.argv:
+        CSRC = os.path.abspath(sys.argv[sys.argv.index("--src") + 1])
+        OUT = os.path.abspath(sys.argv[sys.argv.index("--out") + 1])
+        BUILD = OUT + ".build"
+        build(force=True)
+    else:
+        build(force="--force" in sys.argv)

@@ -484,7 +484,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
               uint32_t off4[8], w8[8];
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                off4[j] = ((wd[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu) * 4u;
+                off4[j] = (j & 1) ? (wd[j >> 1] >> 16) : (wd[j >> 1] & 0xFFFFu);  // stored as byte offsets
                 // byte j & 3 zero-extended in one PRMT (selector nibbles 4 = a zero byte of the second operand)
                 w8[j] = wint8 ? __byte_perm(j < 4 ? S.w.x : S.w.y, 0u, 0x4440u | (uint32_t)(j & 3)) : 1u;
               }
@@ -777,14 +777,20 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
               }
             }
           }
+          if (keep == 0u) {  // the usual case: zero-fill the lane's 4 columns of every row
 #pragma unroll
-          for (int b = 0; b < B; ++b)
-            if (b < nb) {  // zero-fill, except queued pairs (their completion reads and then zeroes them)
-              const uint32_t kb = keep >> (4 * b);
-              *(uint4*)(acc + (size_t)b * TS + col) =
-                  make_uint4(kb & 1u ? v[b][0] : 0u, kb & 2u ? v[b][1] : 0u, kb & 4u ? v[b][2] : 0u,
-                             kb & 8u ? v[b][3] : 0u);
-            }
+            for (int b = 0; b < B; ++b)
+              if (b < nb) *(uint4*)(acc + (size_t)b * TS + col) = make_uint4(0u, 0u, 0u, 0u);
+          } else {
+#pragma unroll
+            for (int b = 0; b < B; ++b)
+              if (b < nb) {  // zero-fill, except queued pairs (their completion reads and then zeroes them)
+                const uint32_t kb = keep >> (4 * b);
+                *(uint4*)(acc + (size_t)b * TS + col) =
+                    make_uint4(kb & 1u ? v[b][0] : 0u, kb & 2u ? v[b][1] : 0u, kb & 4u ? v[b][2] : 0u,
+                               kb & 8u ? v[b][3] : 0u);
+              }
+          }
         }
         flush();
         __syncthreads();
@@ -891,6 +897,9 @@ struct Shape {
 // launches k_accumulate_topk<B, KS, ...> for the shape; defined (explicitly instantiated) in accumulate_ks<KS>.cu
 template <int KS>
 cudaError_t launch_accumulate(const Shape& sh, const QP& p, int sms, cudaStream_t st);
+// the one-row head-free shape runs the warp-specialised bulk-copy kernel (short.cuh, accumulate_short.cu)
+template <int KS>
+cudaError_t launch_short(const QP& p, int sms, cudaStream_t st);
 
 #ifdef KJ_ACCUMULATE_INSTANCES
 namespace {
@@ -916,8 +925,7 @@ cudaError_t launch_main(const QP& p, int sms, cudaStream_t st) {
       if (p.prune_suf || p.residual)  // pruned queries (a6), residual completion (f1)
         return p.vals ? launch_main4<B, KS, true, NW, false, true>(p, sms, st)
                       : launch_main4<B, KS, false, NW, false, true>(p, sms, st);
-      if (!p.head_smem)
-        return p.vals ? launch_main4<B, KS, true, NW, false>(p, sms, st) : launch_main4<B, KS, false, NW, false>(p, sms, st);
+      if (!p.head_smem) return launch_short<KS>(p, sms, st);
     }
     return p.vals ? launch_main4<B, KS, true, NW, true>(p, sms, st) : launch_main4<B, KS, false, NW, true>(p, sms, st);
   } else {

@@ -17,7 +17,9 @@ namespace kj {
 
 constexpr int kMaxK = 256;
 constexpr int kDefaultTile = 8192;
-constexpr int kMaxTile = 32768;        // local ids < tile; padding ids are tile + (0..31) (dummy columns)
+// Posting ids are stored as BYTE offsets of their score column, 4 * (s - tile base) (padding: 4 * (tile + 0..31),
+// dummy columns), so the accumulation kernel adds them to a row base without a shift: 4 * (tile + 32) < 2^16.
+constexpr int kMaxTile = 14336;
 constexpr int kTileQuantum = 2048;     // tile must split into 16 warps' column strips of 128-column steps
 constexpr int kMaxHead = 32;                  // head features per index (one 32-bit word per S row)
 constexpr float kDefaultHeadDensity = 0.125f;  // df >= |S|/8 makes a feature a head candidate

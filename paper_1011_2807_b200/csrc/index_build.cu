@@ -6,8 +6,8 @@
 // and laid out feature-major so that slice (f, t) = I_f ∩ tile t is contiguous:
 //
 //   off[f*(n_tiles+1) + t] .. off[f*(n_tiles+1) + t + 1]   16-byte posting units of slice (f, t)
-//   ids[8*u .. 8*u+8)                                        8 local ids (s - t*tile) per unit; padding
-//                                                            entries hold tile + (u mod 32), a dummy column
+//   ids[8*u .. 8*u+8)                                        8 local ids per unit, as byte offsets 4*(s - t*tile);
+//                                                            padding entries hold 4*(tile + (u mod 32)), dummy columns
 //   vals[8*u .. 8*u+8)                                       INT8 S weights (same positions)
 //
 // Head features.  For BINARY S, the (up to 32) most frequent features with df >= head_density * |S| are
@@ -308,7 +308,7 @@ __global__ void k_units(const uint32_t* __restrict__ counts, uint32_t* __restric
 __global__ void k_fill_pads(uint4* __restrict__ ids, int64_t units, uint32_t tile) {
   int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= units) return;
-  uint32_t pad = tile + (uint32_t)(u & 31);
+  uint32_t pad = (tile + (uint32_t)(u & 31)) << 2;  // byte offset of a dummy column
   pad |= pad << 16;
   ids[u] = make_uint4(pad, pad, pad, pad);
 }
@@ -332,7 +332,7 @@ __global__ void k_scatter(const uint32_t* __restrict__ keys, const VT* __restric
   if (nfull == 0) dst = (rho % m) * 8 + rho / m;  // short slice (one partial block): transpose here
   const size_t pos = (size_t)off[key] * 8 + dst;
   const VT v = vals[i];
-  ids[pos] = (uint16_t)(v & 0xFFFFu);
+  ids[pos] = (uint16_t)((v & 0xFFFFu) << 2);  // byte offset of the score column
   if (wvals) wvals[pos] = sizeof(VT) == 8 ? (WT)(v >> 32) : (WT)(v >> 16);
 }
 
@@ -382,7 +382,7 @@ __global__ void k_block_layout(const uint32_t* __restrict__ off, const uint32_t*
         const bool live = lane < (int)m;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {  // bucket sizes
-          const uint32_t bk = !live ? 33u : (id[j] >= tile ? 32u : (id[j] & 31u));
+          const uint32_t bk = !live ? 33u : (id[j] >= 4 * tile ? 32u : ((id[j] >> 2) & 31u));
           const uint32_t peers = __match_any_sync(0xffffffffu, bk);
           if (bk < 33u && (peers & lt) == 0) cnt[bk] += __popc(peers);
           __syncwarp();
@@ -400,7 +400,7 @@ __global__ void k_block_layout(const uint32_t* __restrict__ off, const uint32_t*
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < 8; ++j) {  // ranks in (slot, lane) order within each bucket
-          const uint32_t bk = !live ? 33u : (id[j] >= tile ? 32u : (id[j] & 31u));
+          const uint32_t bk = !live ? 33u : (id[j] >= 4 * tile ? 32u : ((id[j] >> 2) & 31u));
           const uint32_t peers = __match_any_sync(0xffffffffu, bk);
           const uint32_t start = bk < 33u ? cnt[bk] : 0u;
           dst[j] = start + __popc(peers & lt);

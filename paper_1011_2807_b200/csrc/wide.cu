@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(kWideThreads, 2) k_accumulate_wide(WP p) {
             const uint32_t ww[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
 #pragma unroll
             for (int jj = 0; jj < 8; ++jj) {
-              const uint32_t id = (wd[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu;
+              const uint32_t id = ((wd[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu) >> 2;  // ids are byte offsets
               const double prod = qd * (double)__uint_as_float(ww[jj]);
               if (ww[jj]) atomicAdd(&acc[id], (unsigned long long)rint(prod));
             }
@@ -223,14 +223,14 @@ __global__ void __launch_bounds__(kWideThreads, 2) k_accumulate_wide(WP p) {
             if (p.vals8) w8 = __ldg((const uint2*)(p.vals8 + (size_t)unit * 8));
 #pragma unroll
             for (int jj = 0; jj < 8; ++jj) {
-              const uint32_t id = (wd[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu;
+              const uint32_t id = ((wd[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu) >> 2;  // ids are byte offsets
               const uint32_t w = ((jj < 4 ? w8.x : w8.y) >> (8 * (jj & 3))) & 0xFFu;
               atomicAdd(&acc[id], q * (unsigned long long)w);
             }
           }
           if (p.counters) {
 #pragma unroll
-            for (int jj = 0; jj < 8; ++jj) n_visits += (((wd[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu) < (uint32_t)T) ? 1 : 0;
+            for (int jj = 0; jj < 8; ++jj) n_visits += (((wd[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu) < 4u * (uint32_t)T) ? 1 : 0;
           }
         }
         __syncthreads();

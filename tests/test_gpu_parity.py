@@ -177,6 +177,8 @@ def test_index_layout_matches_scipy_csc(name, T, hd):
     ids_at = al(hc_at + 4 * NT * T)
     cap = st["unit_capacity"]
     ids = raw[ids_at:ids_at + 16 * cap].view(np.uint16)
+    assert np.all(ids % 4 == 0)  # stored as byte offsets of the score columns
+    ids = ids // 4
     vals = None
     if S.values is not None:
         vals_at = al(ids_at + 16 * cap)
