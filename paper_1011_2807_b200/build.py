@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libknnjoin.so")
 BUILD = os.path.join(HERE, "build")
-SOURCES = ["index_build.cu", "query.cu", "merge.cu", "accumulate_ks1.cu", "accumulate_ks4.cu", "accumulate_ks8.cu", "iiib.cu", "wide.cu", "accumulate_short.cu"]
+SOURCES = ["index_build.cu", "query.cu", "merge.cu", "accumulate_ks1.cu", "accumulate_ks4.cu", "accumulate_ks8.cu", "iiib.cu", "wide.cu"]
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v", "--expt-relaxed-constexpr"]

@@ -897,9 +897,6 @@ struct Shape {
 // launches k_accumulate_topk<B, KS, ...> for the shape; defined (explicitly instantiated) in accumulate_ks<KS>.cu
 template <int KS>
 cudaError_t launch_accumulate(const Shape& sh, const QP& p, int sms, cudaStream_t st);
-// the one-row head-free shape runs the warp-specialised bulk-copy kernel (short.cuh, accumulate_short.cu)
-template <int KS>
-cudaError_t launch_short(const QP& p, int sms, cudaStream_t st);
 
 #ifdef KJ_ACCUMULATE_INSTANCES
 namespace {
@@ -925,7 +922,8 @@ cudaError_t launch_main(const QP& p, int sms, cudaStream_t st) {
       if (p.prune_suf || p.residual)  // pruned queries (a6), residual completion (f1)
         return p.vals ? launch_main4<B, KS, true, NW, false, true>(p, sms, st)
                       : launch_main4<B, KS, false, NW, false, true>(p, sms, st);
-      if (!p.head_smem) return launch_short<KS>(p, sms, st);
+      if (!p.head_smem)
+        return p.vals ? launch_main4<B, KS, true, NW, false>(p, sms, st) : launch_main4<B, KS, false, NW, false>(p, sms, st);
     }
     return p.vals ? launch_main4<B, KS, true, NW, true>(p, sms, st) : launch_main4<B, KS, false, NW, true>(p, sms, st);
   } else {
