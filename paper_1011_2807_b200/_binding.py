@@ -11,7 +11,8 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "libknnjoin.so")
+# KNNJOIN_LIB: another build of the same library (the checked build of tools/checked_build.sh); default in-tree
+_SO = os.environ.get("KNNJOIN_LIB") or os.path.join(_HERE, "libknnjoin.so")
 
 BINARY, INT8, FP32 = 0, 1, 2
 _DTYPE_NAMES = {"binary": BINARY, "int8": INT8, "fp32": FP32}
@@ -215,9 +216,10 @@ def _empty_u8(nbytes: int, device) -> torch.Tensor:
 def knnjoin_build_index(S: DeviceCSR, d: int, s_id_base: int = 0, tile: int = 0, stream=None,
                         workspace: torch.Tensor | None = None, head_density: float = 0.0,
                         head_max: int = 0, prune: int = 0, alpha: float = 0.0,
-                        forward: "DeviceCSR | None" = None) -> Index:
+                        forward: "DeviceCSR | None" = None, storage: torch.Tensor | None = None) -> Index:
     """prune=1 keeps S's forward rows for threshold-pruned queries (a6; knnjoin_options.prune / alpha), or the
-    rows of `forward` instead (f1: the residual parts s')."""
+    rows of `forward` instead (f1: the residual parts s').  storage: a caller-provided uint8 device tensor for the
+    index (at least knnjoin_index_bytes; e.g. pre-poisoned by the initialisation tests)."""
     cS = S._c()
     cF = forward._c() if forward is not None else None
     opt = _Options(tile, prune, alpha, head_density, head_max, ctypes.addressof(cF) if cF is not None else 0)
@@ -228,10 +230,11 @@ def knnjoin_build_index(S: DeviceCSR, d: int, s_id_base: int = 0, tile: int = 0,
     if wbytes == 0:
         raise KnnJoinError(1, "knnjoin_build_workspace_bytes", knnjoin_last_error())
     dev = S.indptr.device
-    storage = _empty_u8(nbytes, dev)
+    if storage is None or storage.numel() < nbytes:
+        storage = _empty_u8(nbytes, dev)
     ws = workspace if (workspace is not None and workspace.numel() >= wbytes) else _empty_u8(wbytes, dev)
     out = ctypes.c_void_p()
-    _check(_lib.knnjoin_build_index(ctypes.byref(cS), d, s_id_base, ctypes.byref(opt), storage.data_ptr(), nbytes,
+    _check(_lib.knnjoin_build_index(ctypes.byref(cS), d, s_id_base, ctypes.byref(opt), storage.data_ptr(), storage.numel(),
                                     ws.data_ptr(), ws.numel(), _stream_ptr(stream), ctypes.byref(out)),
            "knnjoin_build_index")
     # keep the workspace alive until the stream has consumed it

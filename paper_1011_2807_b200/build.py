@@ -16,6 +16,8 @@ SOURCES = ["index_build.cu", "query.cu", "merge.cu", "accumulate_ks1.cu", "accum
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
+# checked builds (tools/checked_build.sh): KJ_EXTRA_NVCC_FLAGS="-DKJ_CHECKS" adds the device-side bounds checks
+FLAGS += os.environ.get("KJ_EXTRA_NVCC_FLAGS", "").split()
 
 
 def _compile(src: str) -> str:

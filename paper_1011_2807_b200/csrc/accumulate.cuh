@@ -11,6 +11,7 @@ struct QP {
   // index
   const uint32_t* off;
   const uint16_t* ids;
+  int64_t unit_cap;          // 16-byte units of ids in the index (bounds checks of checked builds)
   const uint8_t* vals;
   const int32_t* head_slot;  // [d] head slot or -1
   const int32_t* head_feat;  // [kMaxHead + 1]; [kMaxHead] = number of head features
@@ -404,6 +405,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
           for (int it = 0; it < IPT; ++it) {
             if (U[it] > 0) {
               const uint32_t c = (uint32_t)(ex >> 32);
+              KJ_CHECK(c < (uint32_t)kCap && (int64_t)u0[it] + U[it] <= p.unit_cap);
               s_ustart[c] = u0[it];
               s_P[c] = (uint32_t)ex;
               s_fm[c] = fm[it];
@@ -473,6 +475,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
               e_cur = min(e_next, n_items - 1);
               if (S.v) {
                 const uint32_t unit = s_ustart[e] + (pp - s_P[e]);
+                KJ_CHECK(e >= 0 && e < n_items && pp >= s_P[e] && pp < s_P[e + 1] && (int64_t)unit < p.unit_cap);
                 S.id = ldg_nc_v4(p.ids + (size_t)unit * 8, l2pol);
                 if (wint8) S.w = ldg_nc_v2(p.vals + (size_t)unit * 8, l2pol);
               }
@@ -485,6 +488,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
                 off4[j] = (j & 1) ? (wd[j >> 1] >> 16) : (wd[j >> 1] & 0xFFFFu);  // stored as byte offsets
+                KJ_CHECK(off4[j] < 4u * (uint32_t)TS && (off4[j] & 3u) == 0);
                 // byte j & 3 zero-extended in one PRMT (selector nibbles 4 = a zero byte of the second operand)
                 w8[j] = wint8 ? __byte_perm(j < 4 ? S.w.x : S.w.y, 0u, 0x4440u | (uint32_t)(j & 3)) : 1u;
               }
@@ -655,6 +659,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
             const uint32_t ent = s_queue[lane];
             pb = (int)(ent >> 16);
             const int cl = (int)(ent & 0xFFFFu);  // column within the tile
+            KJ_CHECK(pb >= 0 && pb < B && cl < T);
             const uint32_t w = __ldg(p.head_cols + (size_t)t * T + cl);
             uint32_t* ap = acc + (size_t)pb * TS + cl;
             uint32_t sc = *ap;
@@ -911,6 +916,7 @@ cudaError_t launch_main4(const QP& p, int sms, cudaStream_t st) {
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   int64_t grid = (int64_t)sms * per_sm;
   if (grid > p.n_batches * p.n_passes) grid = p.n_batches * p.n_passes;
+  grid = checked_grid_cap(grid);
   kern<<<(unsigned)grid, NW * 32, sm, st>>>(p);
   return cudaGetLastError();
 }

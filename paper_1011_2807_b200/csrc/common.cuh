@@ -27,6 +27,26 @@ constexpr int kPadCols = 32;           // dummy score columns per row that absor
 constexpr uint64_t kKeyFloor = 0x00000000FFFFFFFFull;  // score 0 with every id: admits nothing
 constexpr double kFixedOne = 1073741824.0;              // 2^30: per-row fixed-point scale numerator
 
+// Checked builds (-DKJ_CHECKS, tools/checked_build.sh): device-side bounds checks on every index the kernels form
+// into shared and global memory (the stand-in for compute-sanitizer, which this pool does not allow); a failed check
+// prints its site and traps.  KNNJOIN_MAX_CTAS caps the persistent grids so results can be compared across very
+// different schedules (race detection by determinism).  Release builds compile both out.
+#ifdef KJ_CHECKS
+#define KJ_CHECK(cond)                                                                          \
+  do {                                                                                          \
+    if (!(cond)) {                                                                              \
+      printf("KJ_CHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                                \
+      __trap();                                                                                 \
+    }                                                                                           \
+  } while (0)
+#else
+#define KJ_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
+int64_t checked_grid_cap(int64_t grid);  // grid, or min(grid, KNNJOIN_MAX_CTAS) in checked builds
+
 void set_error(const char* fmt, ...);
 knnjoin_status cuda_fail(cudaError_t e, const char* what);
 

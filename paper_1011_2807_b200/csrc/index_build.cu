@@ -331,6 +331,7 @@ __global__ void k_scatter(const uint32_t* __restrict__ keys, const VT* __restric
   uint32_t dst = rho;
   if (nfull == 0) dst = (rho % m) * 8 + rho / m;  // short slice (one partial block): transpose here
   const size_t pos = (size_t)off[key] * 8 + dst;
+  KJ_CHECK(dst < 8 * U && key < sentinel_key);
   const VT v = vals[i];
   ids[pos] = (uint16_t)((v & 0xFFFFu) << 2);  // byte offset of the score column
   if (wvals) wvals[pos] = sizeof(VT) == 8 ? (WT)(v >> 32) : (WT)(v >> 16);

@@ -6,6 +6,7 @@
 // (topk.cuh), so the merge is exact and equals the single-index result bit for bit.  The fixed-point
 // scale of a row depends only on r and the dtype of S, so all ranks produce comparable keys.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -21,6 +22,16 @@ void set_error(const char* fmt, ...) {
   va_start(ap, fmt);
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
+}
+
+int64_t checked_grid_cap(int64_t grid) {
+#ifdef KJ_CHECKS
+  if (const char* s = getenv("KNNJOIN_MAX_CTAS")) {
+    const long long cap = atoll(s);
+    if (cap > 0 && grid > cap) return cap;
+  }
+#endif
+  return grid;
 }
 
 knnjoin_status cuda_fail(cudaError_t e, const char* what) {

@@ -727,6 +727,7 @@ KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr*
     }
     QP p;
     p.off = idx->off;
+    p.unit_cap = idx->unit_cap;
     p.ids = idx->ids;
     p.vals = idx->vals;
     p.head_slot = idx->head_slot;

@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(kWideThreads, 2) k_accumulate_wide(WP p) {
             if (s_P[mid] <= pp) lo = mid; else hi = mid - 1;
           }
           const uint32_t unit = s_u0[lo] + (pp - s_P[lo]);
+          KJ_CHECK(pp >= s_P[lo] && pp < s_P[lo + 1]);
           const uint4 idw = __ldg((const uint4*)(p.ids + (size_t)unit * 8));
           const uint32_t wd[4] = {idw.x, idw.y, idw.z, idw.w};
           if (fp32s) {
@@ -214,6 +215,7 @@ __global__ void __launch_bounds__(kWideThreads, 2) k_accumulate_wide(WP p) {
 #pragma unroll
             for (int jj = 0; jj < 8; ++jj) {
               const uint32_t id = ((wd[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu) >> 2;  // ids are byte offsets
+              KJ_CHECK(id < (uint32_t)(T + kPadCols));
               const double prod = qd * (double)__uint_as_float(ww[jj]);
               if (ww[jj]) atomicAdd(&acc[id], (unsigned long long)rint(prod));
             }
@@ -224,6 +226,7 @@ __global__ void __launch_bounds__(kWideThreads, 2) k_accumulate_wide(WP p) {
 #pragma unroll
             for (int jj = 0; jj < 8; ++jj) {
               const uint32_t id = ((wd[jj >> 1] >> ((jj & 1) * 16)) & 0xFFFFu) >> 2;  // ids are byte offsets
+              KJ_CHECK(id < (uint32_t)(T + kPadCols));
               const uint32_t w = ((jj < 4 ? w8.x : w8.y) >> (8 * (jj & 3))) & 0xFFu;
               atomicAdd(&acc[id], q * (unsigned long long)w);
             }
@@ -427,7 +430,7 @@ cudaError_t launch_wide(const knnjoin_index* idx, const knnjoin_csr* R, int32_t 
   p.out_scores = out_scores;
   p.counters = counters;
   const size_t sm = wide_smem_bytes(idx->tile, k);
-  int64_t grid = wide_ctas(sms);
+  int64_t grid = checked_grid_cap(wide_ctas(sms));
   const int64_t max_items = R->n_rows + (G > 1 ? kWideCapRows * (G - 1) : 0);
   if (grid > max_items) grid = max_items;
   auto go = [&](auto kern) -> cudaError_t {
