@@ -41,7 +41,18 @@ def main():
         cfg = cfg.scaled(a.rows_r or None, a.rows_s or None)
     R, S = gen.generate(cfg, "R"), gen.generate(cfg, "S")
     dR, dS = b.DeviceCSR.from_host(R), b.DeviceCSR.from_host(S)
-    specs = [(x.split(":") + ["0", "0"])[:3] for x in a.libs]  # path[:head_max[:head_density]]
+    # variant spec: path[:key=val,key=val...] with build keys (tile, head_max, head_density) and query keys
+    # (batch_rows, cta_warps, tiles_per_pass, row_order)
+    BUILD = {"tile": int, "head_max": int, "head_density": float}
+    QUERY = {"batch_rows": int, "cta_warps": int, "tiles_per_pass": int, "row_order": int}
+    specs = []
+    for x in a.libs:
+        path, _, opts = x.partition(":")
+        bkw, qkw = {}, {}
+        for kv in filter(None, opts.split(",")):
+            kk, v = kv.split("=")
+            (bkw if kk in BUILD else qkw)[kk] = (BUILD.get(kk) or QUERY[kk])(v)
+        specs.append((path, bkw, qkw))
     libs = [load(sp[0]) for sp in specs]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     times = {p: [] for p in a.libs}
@@ -49,13 +60,13 @@ def main():
     for rep in range(a.reps + 1):
         for p, L, sp in zip(a.libs, libs, specs):
             b._lib = L
-            idx = b.knnjoin_build_index(dS, cfg.d, head_max=int(sp[1]), head_density=float(sp[2]))
+            idx = b.knnjoin_build_index(dS, cfg.d, **sp[1])
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             for e in ev:
                 e.record()
             for q in range(a.queries):
                 flush.fill_(q)
-                b.knnjoin_query(idx, dR, cfg.k, events=ev)
+                b.knnjoin_query(idx, dR, cfg.k, events=ev, **sp[2])
                 torch.cuda.synchronize()
                 if rep > 0:  # rep 0 warms every variant up
                     times[p].append(ev[0].elapsed_time(ev[1]))

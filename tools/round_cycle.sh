@@ -1,24 +1,31 @@
 #!/bin/bash
-# full measurement cycle on the GPU box: parity tests, the default bench line, the launch list and one
-# ncu --set full capture of the accumulate kernel (each ncu pass only after the same command exited 0 without
-# ncu; the .ncu-rep stays in /tmp on the box and is summarised to text here, since gpurun returns <= 64 MiB),
-# plus one bench line per other config.   usage: tools/round_cycle.sh TAG [configs...]
-TAG=${1:-run}; shift
+# Full measurement cycle on the GPU box (tools/round_cycle.sh TAG): GPU tests, smoke, the driver's default bench line
+# (C4), one line per other config, the launch list of the bench command, ncu DRAM traffic of K3 on full C4 and
+# ncu --set full captures (C4-shaped, C2, C3, C5).  Every ncu pass runs only after the same command exited 0 without
+# ncu; summaries go to gpurun_out/ (profiles/ keeps the committed copies).
+TAG=${1:-run}
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu --format=csv > gpurun_out/${TAG}_smi.txt
-timeout 1200 python -m pytest tests -m gpu -q -x --timeout 300 > gpurun_out/${TAG}_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/${TAG}_pytest.log
-timeout 600 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench rc=$?"; head -c 1500 gpurun_out/${TAG}_bench.json; echo
-if timeout 300 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/${TAG}_plain.log 2>&1; then
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv \
-      python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/${TAG}_ncu_launch.log 2>&1; echo "ncu launches rc=$?"
-  rep=/tmp/${TAG}_prof
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_accumulate -s 2 -c 1 -f -o $rep \
-      python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/${TAG}_ncu.log 2>&1; echo "ncu full rc=$?"
-  python tools/ncu_summary.py $rep.ncu-rep 30 > gpurun_out/${TAG}_C2_full.txt 2>&1
-  python tools/ncu_lines.py $rep.ncu-rep 40 >> gpurun_out/${TAG}_C2_full.txt 2>&1
-  ncu -i $rep.ncu-rep --page raw --csv > gpurun_out/${TAG}_C2_raw.csv 2>/dev/null
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu,power.draw --format=csv > gpurun_out/${TAG}_smi.txt
+timeout 2400 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider > gpurun_out/${TAG}_pytest.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/${TAG}_pytest.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/${TAG}_smoke.log
+timeout 1200 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench rc=$?"; head -c 800 gpurun_out/${TAG}_bench.json; echo
+for c in C2 C1 C3 C5; do
+  timeout 900 python bench.py --config $c --steps 10 --warmup 3 > gpurun_out/${TAG}_bench_$c.json 2> gpurun_out/${TAG}_bench_$c.err
+  echo "bench $c rc=$?"
+done
+B="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
+if timeout 900 $B > gpurun_out/${TAG}_plain.log 2>&1; then
+  timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv \
+     $B > gpurun_out/${TAG}_ncu_launch.log 2>&1; echo "ncu launches rc=$?"
+  timeout 1200 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,gpu__time_duration.sum --clock-control none \
+     -k regex:k_accumulate_topk -s 2 -c 1 --csv --log-file gpurun_out/${TAG}_C4_dram.csv $B > gpurun_out/${TAG}_ncu_dram.log 2>&1; echo "ncu dram rc=$?"
 fi
-for c in "$@"; do
-  timeout 900 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/${TAG}_bench_$c.json 2> gpurun_out/${TAG}_bench_$c.err
-  echo "bench $c rc=$?"; head -c 600 gpurun_out/${TAG}_bench_$c.json; echo
+for cfg in "C4 --rows-r 20000 --rows-s 2000000" "C2" "C3" "C5"; do
+  tag=$(echo $cfg | cut -d' ' -f1); [ "$cfg" != "C4" ] && [ "$tag" = "C4" ] && tag=C4s
+  rep=/tmp/${TAG}_$tag
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_accumulate_topk -s 2 -c 1 -f -o $rep \
+     python bench.py --config $cfg --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/${TAG}_ncu_$tag.log 2>&1; echo "ncu full $tag rc=$?"
+  python tools/ncu_summary.py $rep.ncu-rep 30 > gpurun_out/${TAG}_${tag}_full.txt 2>&1
+  python tools/ncu_lines.py $rep.ncu-rep 60 >> gpurun_out/${TAG}_${tag}_full.txt 2>&1
+  python tools/ncu_lines.py $rep.ncu-rep 100 by-inst > gpurun_out/${TAG}_${tag}_byinst.txt 2>&1
 done
