@@ -133,9 +133,24 @@ __host__ __device__ inline size_t staging_at(int B, int T, int k, int NW) { retu
 // an upper bound of the head part of any score whose S row shares p head features with r_b) and
 // head_mask[B] u32 (head slots present in row b).  The per-slot q values they are built from
 // (q_head[kMaxHead][B]) alias the staging area, which is free during batch setup.
-__host__ __device__ inline size_t head_at(int B, int T, int k, int NW) {
-  return align_up(staging_at(B, T, k, NW) + (size_t)kcap(NW) * B * 4 + (size_t)kcap(NW) * 8 +
-                      (size_t)(kcap(NW) + 1) * 4, 16);
+// One-row head-free CTAs (B = 1, no head features: the per-warp path of k_accumulate_topk) use the staging area
+// for per-warp run tables instead: warp w holds the runs [nruns*w/NW, nruns*(w+1)/NW) of the row, kRowRPL per lane
+// in registers, and per tile a table of its non-empty slices -- start P in the warp's flattened unit stream
+// ([kRowCapW + 1] u32) and {first unit - P, q} ([kRowCapW] uint2).
+constexpr int kRowRPL = 6;
+constexpr int kRowCapW = 32 * kRowRPL;
+constexpr int kRowDepth = 3;    // windows whose posting loads are in flight while one is processed
+__host__ __device__ inline size_t row_table_P_bytes() { return align_up((size_t)(kRowCapW + 1) * 4, 16); }
+__host__ __device__ inline size_t row_table_warp_bytes() {
+  return row_table_P_bytes() + (size_t)kRowCapW * 8;
+}
+__host__ __device__ inline size_t staging_bytes(int B, int NW, bool heads) {
+  const size_t chunk = (size_t)kcap(NW) * B * 4 + (size_t)kcap(NW) * 8 + (size_t)(kcap(NW) + 1) * 4;
+  const size_t rows = (B == 1 && !heads) ? (size_t)NW * row_table_warp_bytes() : 0;
+  return chunk > rows ? chunk : rows;
+}
+__host__ __device__ inline size_t head_at(int B, int T, int k, int NW, bool heads) {
+  return align_up(staging_at(B, T, k, NW) + staging_bytes(B, NW, heads), 16);
 }
 // (heads = false: the index has no head features; the head tables and completion queues are left out so that
 // six one-row CTAs fit on an SM)
@@ -143,7 +158,7 @@ __host__ __device__ inline size_t head_bytes(int B, bool heads) {
   return heads ? (size_t)(kMaxHead / 4) * B * 16 * 4 + (size_t)B * (kMaxHead + 1) * 4 + (size_t)B * 4 : 0;
 }
 __host__ __device__ inline size_t tail_at(int B, int T, int k, int NW, bool heads) {
-  return align_up(head_at(B, T, k, NW) + head_bytes(B, heads), 16);
+  return align_up(head_at(B, T, k, NW, heads) + head_bytes(B, heads), 16);
 }
 __host__ __device__ inline size_t smem_bytes(int B, int T, int k, int NW, bool heads) {
   return tail_at(B, T, k, NW, heads) + (size_t)NW * 8 /* scan partials */ + (size_t)B * 8 /* theta */ +
@@ -161,7 +176,7 @@ __device__ __forceinline__ void sts_v4_zero(uint32_t addr) {
 
 
 __device__ __forceinline__ void red_add_shared(uint32_t addr, uint32_t v) {
-  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v));  // ordered by __syncthreads, not by clobbers
 }
 
 
@@ -175,8 +190,10 @@ __device__ __forceinline__ void red_add_shared(uint32_t addr, uint32_t v) {
 // U_N = sum of c over N's non-empty slices of the tile; any other s has score <= x + U_N < theta (or, with
 // x = 0, <= U_N <= budget < theta) and cannot enter.
 template <int B, int KS, bool SINT8, int NW, bool HEADS, bool PRUNE = false>
-__global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_accumulate_topk(QP p) {
+__global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUNE) ? 5 : 6) : (NW == 8 ? 3 : 1))
+    k_accumulate_topk(QP p) {
   static_assert(!PRUNE || (B == 1 && !HEADS), "pruned instances are one-row and head-free");
+  constexpr bool ROWP = B == 1 && !HEADS && !PRUNE;  // one-row head-free instance: per-warp accumulate
   if (p.gate && ((*p.gate > 0) != (p.gate_heads != 0))) return;  // the other candidate shape runs
   constexpr int NT_ = NW * 32;        // threads per CTA
   constexpr int kCap = kcap(NW);      // runs staged per chunk
@@ -191,7 +208,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
   uint32_t* s_ustart = (uint32_t*)(s_q + kCap * QS);
   uint32_t* s_fm = s_ustart + kCap;
   uint32_t* s_P = s_fm + kCap;
-  uint32_t* s_lut = (uint32_t*)(smem + head_at(B, T, p.k, NW));  // [kMaxHead/4][B][16]
+  uint32_t* s_lut = (uint32_t*)(smem + head_at(B, T, p.k, NW, p.head_smem != 0));  // [kMaxHead/4][B][16]
   uint32_t* s_cum = s_lut + (kMaxHead / 4) * B * 16;                 // [B][kMaxHead + 1]
   uint32_t* s_hmask = s_cum + B * (kMaxHead + 1);                    // [B]
   int32_t* s_qh = s_q;                                                // [kMaxHead][B], aliases staging
@@ -346,7 +363,25 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
 #pragma unroll
     for (int it = 0; it < IPT; ++it) {
       const int li = tid + it * NT_;
-      fm_c[it] = (one_chunk && li < kCap && li < nruns) ? __ldg(p.runs_f + run_base + li) : 0u;
+      fm_c[it] = (!ROWP && one_chunk && li < kCap && li < nruns) ? __ldg(p.runs_f + run_base + li) : 0u;
+    }
+    // One-row path (ROWP): warp w takes the runs [wr0, wr1) of the row for every tile -- no block-wide staging.
+    // The first kRowCapW of them stay in registers for the whole item (kRowRPL per lane), and the end of each of
+    // their slices in tile t+1 is loaded while tile t accumulates (a slice of tile t+1 starts where that of tile t
+    // ends: units are feature-major); further runs (rows longer than NW * kRowCapW) are loaded per tile.
+    const int wr0 = ROWP ? (int)(((int64_t)nruns * warp) / NW) : 0;
+    const int wr1 = ROWP ? (int)(((int64_t)nruns * (warp + 1)) / NW) : 0;
+    uint32_t r_o[kRowRPL];                // feature f of each held run (0xFFFFFFFF: none)
+    uint32_t r_s[kRowRPL], r_e[kRowRPL];  // slice of the current tile: units [r_s, r_e) (r_e: loaded ahead)
+    if constexpr (ROWP) {
+#pragma unroll
+      for (int g = 0; g < kRowRPL; ++g) {
+        const int i = wr0 + 32 * g + lane;
+        const bool v = i < wr1 && t_begin < t_stop;
+        r_o[g] = v ? (__ldg(p.runs_f + run_base + i) & 0xFFFFFFu) : 0xFFFFFFFFu;
+        r_s[g] = v ? __ldg(p.off + (size_t)r_o[g] * (size_t)(p.NT + 1) + t_begin) : 0u;
+        r_e[g] = v ? __ldg(p.off + (size_t)r_o[g] * (size_t)(p.NT + 1) + t_begin + 1) : 0u;
+      }
     }
     for (int64_t t = t_begin; t < t_stop; ++t) {
       // a6: the non-essential budget of this tile, from the row's k-th key so far (every thread reads the same
@@ -359,6 +394,148 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : (NW == 8 ? 3 : 1)) k_ac
           budget = a >= (double)(th_s - 1) ? th_s - 1 : (uint32_t)a;
         }
       }
+      if constexpr (ROWP) {
+        // ------------------------------------------------- one-row accumulate (a4): per-warp tables, no barrier
+        unsigned char* wbase = smem + staging_at(B, T, k, NW) + (size_t)warp * row_table_warp_bytes();
+        uint32_t* w_P = (uint32_t*)wbase;                                  // [n_ent + 1] starts
+        uint2* w_bq = (uint2*)(wbase + row_table_P_bytes());               // [n_ent] {first unit - start, q}
+        const uint32_t lt_mask = (1u << lane) - 1u;
+        const int n_sc = (wr1 - wr0 + kRowCapW - 1) / kRowCapW;
+        for (int sc = 0; sc < n_sc; ++sc) {
+          const int cb = wr0 + sc * kRowCapW;  // first run of this super-chunk
+          uint2 cu[kRowRPL];
+          if (sc == 0) {
+#pragma unroll
+            for (int g = 0; g < kRowRPL; ++g) {
+              cu[g] = make_uint2(r_s[g], r_e[g]);
+              if (r_o[g] != 0xFFFFFFFFu) {
+                r_s[g] = r_e[g];
+                if (t + 1 < t_stop) r_e[g] = __ldg(p.off + (size_t)r_o[g] * (size_t)(p.NT + 1) + t + 2);
+              }
+            }
+          } else {  // rows with more than NW * kRowCapW runs: the further super-chunks are loaded per tile
+#pragma unroll
+            for (int g = 0; g < kRowRPL; ++g) {
+              const int i = cb + 32 * g + lane;
+              cu[g] = make_uint2(0u, 0u);
+              if (i < wr1) {
+                const uint32_t* o = p.off + (size_t)(__ldg(p.runs_f + run_base + i) & 0xFFFFFFu) * (size_t)(p.NT + 1) + t;
+                cu[g] = make_uint2(__ldg(o), __ldg(o + 1));
+              }
+            }
+          }
+          // table of the non-empty slices in run order: start P in the warp's unit stream, {first unit - P, q}
+          uint32_t tot = 0, n_ent = 0;
+#pragma unroll
+          for (int g = 0; g < kRowRPL; ++g) {
+            if (cb + 32 * g < wr1) {  // warp-uniform
+              const uint32_t L = cu[g].y - cu[g].x;
+              uint32_t incl = L;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+              }
+              const uint32_t ne = __ballot_sync(0xffffffffu, L > 0);
+              if (L > 0) {
+                const uint32_t c = n_ent + __popc(ne & lt_mask);
+                const uint32_t P = tot + incl - L;
+                KJ_CHECK(c < (uint32_t)kRowCapW && (int64_t)cu[g].y <= p.unit_cap);
+                w_P[c] = P;
+                w_bq[c] = make_uint2(cu[g].x - P, (uint32_t)__ldg(p.runs_q + run_base + cb + 32 * g + lane));
+              }
+              tot += __shfl_sync(0xffffffffu, incl, 31);
+              n_ent += __popc(ne);
+            }
+          }
+          if (lane == 0) w_P[n_ent] = tot;
+          __syncwarp();
+          phase_mark(0);
+          const uint32_t wend = (tot + 31) >> 5;
+          if (wend) {
+            // software pipeline over the windows of 32 units (lane l takes unit 32m + l): R (the entries starting
+            // inside window m, one OR-reduction of the next 32 starts past e_cur, the entry covering its first
+            // unit) -> C (posting loads) -> process.  Every stage consumes shared-memory results loaded one step
+            // earlier, so no step waits on a load issued in the same step; kRowDepth windows' posting loads are in
+            // flight while one is processed.
+            struct St {
+              uint4 id;
+              uint2 w;
+              uint32_t q;
+              bool v;
+            };
+            const int n_items = (int)n_ent;
+            int e_cur = 0;  // entry covering the first unit of the next window stage R handles
+            auto ldP = [&]() { return w_P[min(e_cur + 1 + lane, n_items)]; };
+            // stage R for window m: pS = starts after e_cur (loaded one step earlier); returns {first unit - start,
+            // q} of lane l's entry (a shared load consumed one step later) and advances e_cur, reloading pS
+            auto stR = [&](uint32_t m, uint32_t& pS) -> uint2 {
+              if (m >= wend) return make_uint2(0u, 0u);
+              const uint32_t o = pS - m * 32;  // >= 1: e_cur covers unit 32m, so the next start lies past it
+              const uint32_t M = __reduce_or_sync(0xffffffffu, o < 32 ? (1u << o) : 0u);
+              const int e = e_cur + __popc(M & (lt_mask | (1u << lane)));
+              const int e_next = e_cur + __popc(M) + (__ballot_sync(0xffffffffu, o == 32) ? 1 : 0);
+              e_cur = min(e_next, n_items - 1);
+              KJ_CHECK(e >= 0 && e < n_items);
+              const uint2 bq = w_bq[min(e, n_items - 1)];
+              pS = ldP();
+              return bq;
+            };
+            auto stC = [&](uint32_t m, uint2 bq, St& S) {
+              const uint32_t pp = m * 32 + lane;
+              S.v = m < wend && pp < tot;
+              if (S.v) {
+                const uint32_t unit = bq.x + pp;
+                KJ_CHECK((int64_t)unit < p.unit_cap);
+                S.q = bq.y;
+                S.id = ldg_nc_v4(p.ids + (size_t)unit * 8, l2pol);
+                if (wint8) S.w = ldg_nc_v2(p.vals + (size_t)unit * 8, l2pol);
+              }
+            };
+            auto process = [&](const St& S) {
+              if (!S.v) return;
+              const uint32_t wd[4] = {S.id.x, S.id.y, S.id.z, S.id.w};
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const uint32_t o4 = (j & 1) ? (wd[j >> 1] >> 16) : (wd[j >> 1] & 0xFFFFu);  // byte offsets
+                KJ_CHECK(o4 < 4u * (uint32_t)TS && (o4 & 3u) == 0);
+                const uint32_t w8 = wint8 ? __byte_perm(j < 4 ? S.w.x : S.w.y, 0u, 0x4440u | (uint32_t)(j & 3)) : 1u;
+                red_add_shared(acc_s + o4, wint8 ? S.q * w8 : S.q);
+              }
+              if (p.counters) {
+                int nid = 0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) nid += ((j & 1) ? (wd[j >> 1] >> 16) : (wd[j >> 1] & 0xFFFFu)) < (uint32_t)T * 4u;
+                n_visits += (unsigned long long)nid;
+              }
+            };
+            constexpr int LD = kRowDepth;  // windows whose loads are in flight
+            St D[LD + 1];
+#pragma unroll
+            for (int j = 0; j <= LD; ++j) {
+              D[j].id = make_uint4(0, 0, 0, 0);
+              D[j].w = make_uint2(0, 0);
+              D[j].q = 0;
+              D[j].v = false;
+            }
+            uint32_t pS = ldP();
+#pragma unroll
+            for (int j = 0; j < LD; ++j) stC(j, stR(j, pS), D[j]);
+            uint2 bqC = stR(LD, pS);
+            for (uint32_t w = 0; w < wend; w += LD + 1) {
+#pragma unroll
+              for (int j = 0; j <= LD; ++j) {
+                stC(w + j + LD, bqC, D[(j + LD) % (LD + 1)]);
+                bqC = stR(w + j + LD + 1, pS);
+                process(D[j]);
+              }
+            }
+          }
+          __syncwarp();  // table reads done before the next super-chunk rewrites it
+        }
+        __syncthreads();
+        phase_mark(1);
+      } else
       for (int c0 = 0; c0 < nruns; c0 += kCap) {
         // ---------------------------------------------------------------- stage chunk of runs
         // non-empty slices are compacted with their position P in the flattened unit stream (head

@@ -355,7 +355,7 @@ bool pick_shape(int T, int k, int req_B, int req_NW, int heads, Shape* out) {
     return false;
   }
   if (heads == 0)
-    for (int ctas : {6, 5, 4})
+    for (int ctas : {6, 5, 4, 3})
       if (fits(1, 4, ctas)) { *out = {1, 4}; return true; }
   for (int B : Bs)
     if (B >= 2 && fits(B, 8, 3)) { *out = {B, 8}; return true; }

@@ -50,6 +50,10 @@ def sass(rep, top=25):
         wi = sum(int(r[ix['L1 Wavefronts Shared Ideal']] or 0) for r in sel)
         n = sum(int(r[ix['Instructions Executed']] or 0) for r in sel)
         print(f"  {kind}: instr {n:.3e} wavefronts {wf:.3e} ideal {wi:.3e} ({wf / max(n, 1):.2f}/instr)")
+    print("top SASS by shared wavefronts:")
+    for r in sorted(data, key=lambda r: -int(r[ix['L1 Wavefronts Shared']] or 0))[:12]:
+        print(f"  {r[0][-5:]} {r[1][:58]:58s} wf {r[ix['L1 Wavefronts Shared']]:>11s} ideal "
+              f"{r[ix['L1 Wavefronts Shared Ideal']]:>11s} inst {r[ix['Instructions Executed']]:>11s}")
     print("hottest lines:")
     for r in sorted(data, key=lambda r: -int(r[ix['Warp Stall Sampling (All Samples)']] or 0))[:top]:
         st = sorted(((int(r[ix[h]] or 0), h[6:]) for h in stalls), reverse=True)[:2]
