@@ -84,6 +84,20 @@ __device__ __forceinline__ uint2 ldg_nc_v2(const void* p, uint64_t pol) {
   return r;
 }
 
+// Streaming data read once per work item (a one-row item's runs): L2 evict-first, so that it does not push the
+// pass slab of the index out of L2.  (The top-k state carried between passes keeps the default policy: evict-
+// first on it measured 2-3 % slower on C2 / C4, whose items wait for it at entry.)
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint32_t ldg_stream_u32(const void* p, uint64_t pol) {
+  uint32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
+
 namespace {
 
 // -------------------------------------------------------------------------- block-wide scan helper
@@ -139,7 +153,7 @@ __host__ __device__ inline size_t staging_at(int B, int T, int k, int NW) { retu
 // ([kRowCapW + 1] u32) and {first unit - P, q} ([kRowCapW] uint2).
 constexpr int kRowRPL = 6;
 constexpr int kRowCapW = 32 * kRowRPL;
-constexpr int kRowDepth = 3;    // windows whose posting loads are in flight while one is processed
+constexpr int kRowDepth = 2;    // windows whose posting loads are in flight while one is processed
 __host__ __device__ inline size_t row_table_P_bytes() { return align_up((size_t)(kRowCapW + 1) * 4, 16); }
 __host__ __device__ inline size_t row_table_warp_bytes() {
   return row_table_P_bytes() + (size_t)kRowCapW * 8;
@@ -236,6 +250,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
   };
   unsigned long long n_visits = 0, n_inserts = 0, n_complete = 0, n_skipped = 0;
   const uint64_t l2pol = l2_policy_normal();
+  const uint64_t l2first = l2_policy_first();
   const int n_head = (HEADS && p.head_smem) ? p.head_feat[kMaxHead] : 0;  // host: head_smem when n_head > 0
   const int n_groups = HEADS ? (n_head + 3) >> 2 : 0;
 
@@ -372,13 +387,15 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
     const int wr0 = ROWP ? (int)(((int64_t)nruns * warp) / NW) : 0;
     const int wr1 = ROWP ? (int)(((int64_t)nruns * (warp + 1)) / NW) : 0;
     uint32_t r_o[kRowRPL];                // feature f of each held run (0xFFFFFFFF: none)
+    uint32_t r_q[kRowRPL];                // its q
     uint32_t r_s[kRowRPL], r_e[kRowRPL];  // slice of the current tile: units [r_s, r_e) (r_e: loaded ahead)
     if constexpr (ROWP) {
 #pragma unroll
       for (int g = 0; g < kRowRPL; ++g) {
         const int i = wr0 + 32 * g + lane;
         const bool v = i < wr1 && t_begin < t_stop;
-        r_o[g] = v ? (__ldg(p.runs_f + run_base + i) & 0xFFFFFFu) : 0xFFFFFFFFu;
+        r_o[g] = v ? (ldg_stream_u32(p.runs_f + run_base + i, l2first) & 0xFFFFFFu) : 0xFFFFFFFFu;
+        r_q[g] = v ? ldg_stream_u32(p.runs_q + run_base + i, l2first) : 0u;
         r_s[g] = v ? __ldg(p.off + (size_t)r_o[g] * (size_t)(p.NT + 1) + t_begin) : 0u;
         r_e[g] = v ? __ldg(p.off + (size_t)r_o[g] * (size_t)(p.NT + 1) + t_begin + 1) : 0u;
       }
@@ -404,10 +421,12 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
         for (int sc = 0; sc < n_sc; ++sc) {
           const int cb = wr0 + sc * kRowCapW;  // first run of this super-chunk
           uint2 cu[kRowRPL];
+          uint32_t cq[kRowRPL];
           if (sc == 0) {
 #pragma unroll
             for (int g = 0; g < kRowRPL; ++g) {
               cu[g] = make_uint2(r_s[g], r_e[g]);
+              cq[g] = r_q[g];
               if (r_o[g] != 0xFFFFFFFFu) {
                 r_s[g] = r_e[g];
                 if (t + 1 < t_stop) r_e[g] = __ldg(p.off + (size_t)r_o[g] * (size_t)(p.NT + 1) + t + 2);
@@ -418,6 +437,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
             for (int g = 0; g < kRowRPL; ++g) {
               const int i = cb + 32 * g + lane;
               cu[g] = make_uint2(0u, 0u);
+              cq[g] = i < wr1 ? __ldg(p.runs_q + run_base + i) : 0u;
               if (i < wr1) {
                 const uint32_t* o = p.off + (size_t)(__ldg(p.runs_f + run_base + i) & 0xFFFFFFu) * (size_t)(p.NT + 1) + t;
                 cu[g] = make_uint2(__ldg(o), __ldg(o + 1));
@@ -442,7 +462,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
                 const uint32_t P = tot + incl - L;
                 KJ_CHECK(c < (uint32_t)kRowCapW && (int64_t)cu[g].y <= p.unit_cap);
                 w_P[c] = P;
-                w_bq[c] = make_uint2(cu[g].x - P, (uint32_t)__ldg(p.runs_q + run_base + cb + 32 * g + lane));
+                w_bq[c] = make_uint2(cu[g].x - P, cq[g]);
               }
               tot += __shfl_sync(0xffffffffu, incl, 31);
               n_ent += __popc(ne);
