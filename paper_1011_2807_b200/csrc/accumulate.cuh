@@ -159,7 +159,8 @@ __host__ __device__ inline size_t row_table_warp_bytes() {
   return row_table_P_bytes() + (size_t)kRowCapW * 8;
 }
 __host__ __device__ inline size_t staging_bytes(int B, int NW, bool heads) {
-  const size_t chunk = (size_t)kcap(NW) * B * 4 + (size_t)kcap(NW) * 8 + (size_t)(kcap(NW) + 1) * 4;
+  // (B <= 2: one 16-byte record {first unit - start, feature | row mask, q0, q1} per staged run, then the starts)
+  const size_t chunk = (size_t)kcap(NW) * (B > 2 ? B : 2) * 4 + (size_t)kcap(NW) * 8 + (size_t)(kcap(NW) + 1) * 4;
   const size_t rows = (B == 1 && !heads) ? (size_t)NW * row_table_warp_bytes() : 0;
   return chunk > rows ? chunk : rows;
 }
@@ -222,6 +223,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
   uint32_t* s_ustart = (uint32_t*)(s_q + kCap * QS);
   uint32_t* s_fm = s_ustart + kCap;
   uint32_t* s_P = s_fm + kCap;
+  uint4* s_ent = (uint4*)s_q;                // B <= 2: staged run records {first unit - start, fm, q0, q1}
+  uint32_t* s_P2 = (uint32_t*)(s_ent + kCap);  //   and their starts (+ the total at [n])
   uint32_t* s_lut = (uint32_t*)(smem + head_at(B, T, p.k, NW, p.head_smem != 0));  // [kMaxHead/4][B][16]
   uint32_t* s_cum = s_lut + (kMaxHead / 4) * B * 16;                 // [B][kMaxHead + 1]
   uint32_t* s_hmask = s_cum + B * (kMaxHead + 1);                    // [B]
@@ -603,12 +606,19 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
             if (U[it] > 0) {
               const uint32_t c = (uint32_t)(ex >> 32);
               KJ_CHECK(c < (uint32_t)kCap && (int64_t)u0[it] + U[it] <= p.unit_cap);
-              s_ustart[c] = u0[it];
-              s_P[c] = (uint32_t)ex;
-              s_fm[c] = fm[it];
               const size_t run = (size_t)(run_base + c0 + tid + it * NT_);
+              if constexpr (B <= 2) {
+                const uint32_t P = (uint32_t)ex;
+                s_ent[c] = make_uint4(u0[it] - P, fm[it], (uint32_t)p.runs_q[run * B],
+                                      B == 2 ? (uint32_t)p.runs_q[run * B + 1] : 0u);
+                s_P2[c] = P;
+              } else {
+                s_ustart[c] = u0[it];
+                s_P[c] = (uint32_t)ex;
+                s_fm[c] = fm[it];
 #pragma unroll
-              for (int b = 0; b < B; ++b) s_q[c * QS + b] = p.runs_q[run * B + b];
+                for (int b = 0; b < B; ++b) s_q[c * QS + b] = p.runs_q[run * B + b];
+              }
             }
             ex += pk[it];
           }
@@ -616,7 +626,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
             const uint32_t ns = (uint32_t)(total >> 32);
             s_misc[1] = (int)ns;
             s_misc[2] = (int)(uint32_t)total;
-            s_P[ns] = (uint32_t)total;
+            if constexpr (B <= 2) s_P2[ns] = (uint32_t)total;
+            else s_P[ns] = (uint32_t)total;
           }
           __syncthreads();
           phase_mark(0);
@@ -635,11 +646,98 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
             const uint32_t w1 = (uint32_t)(((uint64_t)nwin * (warp + 1)) / NW);
             if (w0 < w1) {
             const uint32_t p_begin = w0 * 32, p_end = min(TOT, w1 * 32);
+            const uint32_t* sP = B <= 2 ? s_P2 : s_P;
             int lo = 0, hi = n_items - 1;  // largest e with P[e] <= p_begin
             while (lo < hi) {
               int mid = (lo + hi + 1) >> 1;
-              if (s_P[mid] <= p_begin) lo = mid; else hi = mid - 1;
+              if (sP[mid] <= p_begin) lo = mid; else hi = mid - 1;
             }
+            if constexpr (B <= 2) {
+              // software pipeline (as in the one-row path): R (entry of each lane: one OR-reduction of the next 32
+              // starts past e_cur; the record load) -> C (posting loads) -> process, each stage consuming shared
+              // loads issued one step earlier
+              int e_cur = lo;
+              struct St2 {
+                uint4 id;
+                uint2 w;
+                uint32_t fm, q0, q1;
+                bool v;
+              };
+              const uint32_t le_mask = (2u << lane) - 1u;
+              auto ldP = [&]() { return s_P2[min(e_cur + 1 + lane, n_items)]; };
+              auto stR = [&](uint32_t p0, uint32_t& pS) -> uint4 {
+                if (p0 >= p_end) return make_uint4(0u, 0u, 0u, 0u);
+                const uint32_t o = pS - p0;  // >= 1
+                const uint32_t M = __reduce_or_sync(0xffffffffu, o < 32 ? (1u << o) : 0u);
+                const int e = e_cur + __popc(M & le_mask);
+                const int e_next = e_cur + __popc(M) + (__ballot_sync(0xffffffffu, o == 32) ? 1 : 0);
+                e_cur = min(e_next, n_items - 1);
+                KJ_CHECK(e >= 0 && (e < n_items || p0 + lane >= p_end));
+                const uint4 ent = s_ent[min(e, n_items - 1)];
+                pS = ldP();
+                return ent;
+              };
+              auto stC = [&](uint32_t p0, const uint4& ent, St2& S) {
+                const uint32_t pp = p0 + lane;
+                S.v = p0 < p_end && pp < p_end;
+                if (S.v) {
+                  const uint32_t unit = ent.x + pp;
+                  KJ_CHECK((int64_t)unit < p.unit_cap);
+                  S.fm = ent.y >> 24;
+                  S.q0 = ent.z;
+                  S.q1 = ent.w;
+                  S.id = ldg_nc_v4(p.ids + (size_t)unit * 8, l2pol);
+                  if (wint8) S.w = ldg_nc_v2(p.vals + (size_t)unit * 8, l2pol);
+                }
+              };
+              auto process2 = [&](const St2& S) {
+                if (!S.v) return;
+                const uint32_t wd[4] = {S.id.x, S.id.y, S.id.z, S.id.w};
+                uint32_t off4[8], w8[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  off4[j] = (j & 1) ? (wd[j >> 1] >> 16) : (wd[j >> 1] & 0xFFFFu);
+                  KJ_CHECK(off4[j] < 4u * (uint32_t)TS && (off4[j] & 3u) == 0);
+                  w8[j] = wint8 ? __byte_perm(j < 4 ? S.w.x : S.w.y, 0u, 0x4440u | (uint32_t)(j & 3)) : 1u;
+                }
+#pragma unroll
+                for (int b = 0; b < B; ++b) {
+                  if (S.fm & (1u << b)) {
+                    const uint32_t q = b == 0 ? S.q0 : S.q1;
+                    const uint32_t rb = acc_s + (uint32_t)(b * TS * 4);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) red_add_shared(rb + off4[j], wint8 ? q * w8[j] : q);
+                  }
+                }
+                if (p.counters) {
+                  int nid = 0;
+#pragma unroll
+                  for (int j = 0; j < 8; ++j) nid += off4[j] < (uint32_t)T * 4u;
+                  n_visits += (unsigned long long)nid * __popc(S.fm & ((1u << B) - 1u));
+                }
+              };
+              constexpr int LD = B == 1 ? 2 : 1;  // windows whose posting loads are in flight
+              St2 D[LD + 1];
+#pragma unroll
+              for (int j = 0; j <= LD; ++j) {
+                D[j].id = make_uint4(0, 0, 0, 0);
+                D[j].w = make_uint2(0, 0);
+                D[j].fm = D[j].q0 = D[j].q1 = 0;
+                D[j].v = false;
+              }
+              uint32_t pS = ldP();
+#pragma unroll
+              for (int j = 0; j < LD; ++j) stC(p_begin + 32 * j, stR(p_begin + 32 * j, pS), D[j]);
+              uint4 entC = stR(p_begin + 32 * LD, pS);
+              for (uint32_t p0 = p_begin; p0 < p_end; p0 += 32 * (LD + 1)) {
+#pragma unroll
+                for (int j = 0; j <= LD; ++j) {
+                  stC(p0 + 32 * (j + LD), entC, D[(j + LD) % (LD + 1)]);
+                  entC = stR(p0 + 32 * (j + LD + 1), pS);
+                  process2(D[j]);
+                }
+              }
+            } else {
             int e_cur = lo;
             struct Stage {
               uint4 id;
@@ -726,6 +824,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
                 A = Bs;
               }
             }
+            }  // B > 2
             }
           }
           __syncthreads();
