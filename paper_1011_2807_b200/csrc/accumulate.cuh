@@ -982,6 +982,9 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
           }
           qn = 0;
         };
+        uint32_t hmr[B];  // head slots present in each row (constant over the item)
+#pragma unroll
+        for (int b = 0; b < B; ++b) hmr[b] = n_groups ? s_hmask[b] : 0u;
         if (n_groups)
         for (int c = 0; c < cols; c += 128) {
           const int col = cbase + c + lane * 4;
@@ -1007,7 +1010,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
               if (b < nb) {
                 th[b] = row_theta(b);
                 const uint32_t t32 = t32_of(th[b]);
-                const uint32_t hm = s_hmask[b];
+                const uint32_t hm = hmr[b];
                 const uint32_t* cum = s_cum + b * (kMaxHead + 1);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {

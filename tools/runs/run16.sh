@@ -1,0 +1,2 @@
+for c in C2; do timeout 600 python tools/ab.py --config $c --reps 3 ab_libs/v5.so paper_1011_2807_b200/libknnjoin.so 2>&1 | tail -2; done
+timeout 600 python tools/ab.py --config C4 --rows-r 20000 --rows-s 2000000 --reps 1 ab_libs/v5.so paper_1011_2807_b200/libknnjoin.so 2>&1 | tail -2
