@@ -87,9 +87,14 @@ bool index_layout(const knnjoin_csr* S, int32_t d, int32_t tile, bool prune, Ind
 namespace {
 
 struct BuildWs {
-  size_t counts_at, units_at, first_at, ka_at, kb_at, va_at, vb_at, cub_at,
+  size_t counts_at, units_at, first_at, endp_at, ka_at, kb_at, va_at, vb_at, cub_at,
       cub_bytes, total;
 };
+
+// the feature-key build applies (see k_keys_f)
+bool use_fkey(const knnjoin_csr* S) {
+  return S->dtype == KNNJOIN_BINARY || (S->dtype == KNNJOIN_INT8 && S->n_rows < ((int64_t)1 << 24));
+}
 
 int end_bit_for(int64_t max_key) {
   int b = 1;
@@ -114,6 +119,7 @@ bool build_ws_layout(const knnjoin_csr* S, int32_t d, const IndexLayout& L, Buil
   W->counts_at = at; at = align_up(at + 4 * n_off, 256);
   W->units_at = at;  at = align_up(at + 4 * n_off, 256);
   W->first_at = at;  at = align_up(at + 4 * n_off, 256);
+  W->endp_at = at;   at = align_up(at + 4 * n_off, 256);
   W->ka_at = at;     at = align_up(at + 4 * nnz, 256);
   W->kb_at = at;     at = align_up(at + 4 * nnz, 256);
   // sort values: (local id | int8 weight << 16) as u32, or (local id | fp32 weight bits << 32) as u64 (FP32 S)
@@ -206,6 +212,66 @@ __global__ void k_seg_count(const uint32_t* __restrict__ keys, int64_t nnz, uint
   if (i >= nnz) return;
   uint32_t k = keys[i];
   if (k < sentinel_key && (i == nnz - 1 || keys[i + 1] != k)) counts[k] = (uint32_t)(i + 1) - first[k];
+}
+
+// ---- feature-key build (BINARY S, INT8 S with < 2^24 rows): the CSR is in row order, so a STABLE sort by the
+// feature alone yields (feature, row) order -- the (feature, tile, row) order of the slice keys -- with
+// ceil(log2(d + 1)) key bits instead of those of f * (n_tiles + 1) + t (one radix pass fewer at C4's sizes).
+// Sort value: the row s (BINARY) or s << 8 | weight (INT8); the slice key is recomputed from (f, s / tile).
+__global__ void k_keys_f(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                         const void* __restrict__ values, int64_t n_s, int32_t d, uint32_t* __restrict__ keys,
+                         uint32_t* __restrict__ vals) {
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n_s) return;
+  for (int64_t j = indptr[row] + lane; j < indptr[row + 1]; j += 32) {
+    const int32_t f = indices[j];
+    keys[j] = (f >= 0 && f < d) ? (uint32_t)f : (uint32_t)d;  // invalid features sort last (key d)
+    vals[j] = values ? ((uint32_t)row << 8) | (uint32_t)(uint8_t)((const int8_t*)values)[j] : (uint32_t)row;
+  }
+}
+
+__device__ __forceinline__ uint32_t fkey_slice(uint32_t f, uint32_t v, int wshift, uint32_t tile, int64_t n_tiles) {
+  return (uint32_t)((int64_t)f * (n_tiles + 1) + (v >> wshift) / tile);
+}
+
+// segment bounds of every present slice key: first[key] = first sorted position, endp[key] = one past the last
+// (both memset 0, so absent keys have count endp - first = 0)
+__global__ void k_seg_f(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, int64_t nnz, int32_t d,
+                        int wshift, uint32_t tile, int64_t n_tiles, uint32_t* __restrict__ first,
+                        uint32_t* __restrict__ endp) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nnz) return;
+  const uint32_t f = keys[i];
+  if (f >= (uint32_t)d) return;
+  const uint32_t k = fkey_slice(f, vals[i], wshift, tile, n_tiles);
+  if (i == 0 || keys[i - 1] != f || fkey_slice(f, vals[i - 1], wshift, tile, n_tiles) != k) first[k] = (uint32_t)i;
+  if (i == nnz - 1 || keys[i + 1] != f || fkey_slice(f, vals[i + 1], wshift, tile, n_tiles) != k) endp[k] = (uint32_t)(i + 1);
+}
+
+__global__ void k_counts_f(const uint32_t* __restrict__ first, const uint32_t* __restrict__ endp, int64_t n,
+                           uint32_t* __restrict__ counts) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) counts[i] = endp[i] - first[i];
+}
+
+// posting of sorted rank rho goes to position rho of its slice (k_block_layout permutes inside blocks)
+__global__ void k_scatter_f(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, int64_t nnz,
+                            int32_t d, int wshift, uint32_t tile, int64_t n_tiles, const uint32_t* __restrict__ off,
+                            const uint32_t* __restrict__ first, const uint32_t* __restrict__ units,
+                            uint16_t* __restrict__ ids, uint8_t* __restrict__ wvals) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nnz) return;
+  const uint32_t f = keys[i];
+  if (f >= (uint32_t)d) return;
+  const uint32_t v = vals[i], srow = v >> wshift, t = srow / tile;
+  const uint32_t k = (uint32_t)((int64_t)f * (n_tiles + 1) + t);
+  if (units[k] == 0) return;  // head feature
+  const uint32_t dst = (uint32_t)i - first[k];
+  KJ_CHECK(dst < 8 * units[k]);
+  const size_t pos = (size_t)off[k] * 8 + dst;
+  ids[pos] = (uint16_t)((srow - t * tile) << 2);  // byte offset of the score column
+  if (wvals) wvals[pos] = (uint8_t)(v & 0xFFu);
 }
 
 // warp per feature: df[f] = sum over tiles of counts[f][t]; also the (df, f) pairs for head selection
@@ -454,12 +520,28 @@ __global__ void k_fmax(const int32_t* __restrict__ indices, const int8_t* __rest
 
 // the largest weight of S (u32 for INT8; float bits for FP32 -- positive floats order like their bits): the
 // 64-bit fixed-point scale of wide queries (wide.cu) keeps every partial score below 2^62 with it
-__global__ void k_wmax(const void* __restrict__ values, knnjoin_dtype dt, int64_t nnz, uint32_t* __restrict__ wmax) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// (grid-stride, one atomic per CTA: a per-warp atomic on the one word serialises at L2 -- 7.7 ms on C5's 375 M
+// weights, measured)
+__global__ void __launch_bounds__(256) k_wmax(const void* __restrict__ values, knnjoin_dtype dt, int64_t nnz,
+                                              uint32_t* __restrict__ wmax) {
+  __shared__ uint32_t s_max[8];
   uint32_t v = 0;
-  if (i < nnz) v = dt == KNNJOIN_FP32 ? __float_as_uint(((const float*)values)[i]) : (uint32_t)(uint8_t)((const int8_t*)values)[i];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (dt == KNNJOIN_FP32) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += stride)
+      v = max(v, __float_as_uint(((const float*)values)[i]));
+  } else {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += stride)
+      v = max(v, (uint32_t)(uint8_t)((const int8_t*)values)[i]);
+  }
   v = __reduce_max_sync(0xffffffffu, v);
-  if ((threadIdx.x & 31) == 0 && v) atomicMax(wmax, v);
+  if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = threadIdx.x < (blockDim.x >> 5) ? s_max[threadIdx.x] : 0u;
+    v = __reduce_max_sync(0xffffffffu, v);
+    if (threadIdx.x == 0 && v) atomicMax(wmax, v);
+  }
 }
 
 }  // namespace
@@ -556,11 +638,33 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   if (S->dtype == KNNJOIN_BINARY) {
     if ((e = cudaMemsetAsync(wmax, 0x01, 1, st)) != cudaSuccess) return cuda_fail(e, "wmax");  // weight 1
   } else if (S->nnz > 0) {
-    k_wmax<<<(unsigned)((S->nnz + 255) / 256), 256, 0, st>>>(S->values, S->dtype, S->nnz, wmax);
+    {
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const int64_t want = (S->nnz + 255) / 256, cap = (int64_t)sms * 8;
+      k_wmax<<<(unsigned)(want < cap ? want : cap), 256, 0, st>>>(S->values, S->dtype, S->nnz, wmax);
+    }
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_wmax");
   }
   const unsigned gnnz = (unsigned)((S->nnz + 255) / 256);
-  if (S->nnz > 0) {
+  const bool fkey = use_fkey(S);
+  const int wshift = S->dtype == KNNJOIN_INT8 ? 8 : 0;
+  uint32_t* endp = (uint32_t*)(wb + W.endp_at);
+  if (fkey && S->nnz > 0) {
+    if ((e = cudaMemsetAsync(first, 0, 4 * (size_t)L.n_off, st)) != cudaSuccess) return cuda_fail(e, "memset first");
+    if ((e = cudaMemsetAsync(endp, 0, 4 * (size_t)L.n_off, st)) != cudaSuccess) return cuda_fail(e, "memset endp");
+    const int64_t threads = S->n_rows * 32;
+    k_keys_f<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(S->indptr, S->indices, wshift ? S->values : nullptr,
+                                                                S->n_rows, d, ka, va);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_keys_f");
+    size_t tb = W.cub_bytes;
+    if ((e = cub::DeviceRadixSort::SortPairs(cubtmp, tb, ka, kb, va, vb, (int)S->nnz, 0, end_bit_for(d), st)) != cudaSuccess)
+      return cuda_fail(e, "radix sort");
+    k_seg_f<<<gnnz, 256, 0, st>>>(kb, vb, S->nnz, d, wshift, (uint32_t)tile, L.n_tiles, first, endp);
+    k_counts_f<<<(unsigned)((L.n_off + 255) / 256), 256, 0, st>>>(first, endp, L.n_off, counts);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_seg_f");
+  } else if (S->nnz > 0) {
     int64_t threads = S->n_rows * 32;
     if (f32)
       k_keys<uint64_t><<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(S->indptr, S->indices, S->values, S->n_rows, d,
@@ -589,7 +693,9 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
   k_fill_pads<<<(unsigned)((L.unit_cap + 255) / 256), 256, 0, st>>>((uint4*)ids, L.unit_cap, (uint32_t)tile);
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "k_fill_pads");
   if (S->nnz > 0) {
-    if (f32)
+    if (fkey)
+      k_scatter_f<<<gnnz, 256, 0, st>>>(kb, vb, S->nnz, d, wshift, (uint32_t)tile, L.n_tiles, off, first, units, ids, vals);
+    else if (f32)
       k_scatter<<<gnnz, 256, 0, st>>>(kb, vb64, S->nnz, off, first, units, sentinel_key, ids, vals32);
     else
       k_scatter<<<gnnz, 256, 0, st>>>(kb, vb, S->nnz, off, first, units, sentinel_key, ids, vals);
