@@ -57,6 +57,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     times = {p: [] for p in a.libs}
     orig = b._lib
+    ref_keys, mismatch = None, set()
     for rep in range(a.reps + 1):
         for p, L, sp in zip(a.libs, libs, specs):
             b._lib = L
@@ -66,8 +67,15 @@ def main():
                 e.record()
             for q in range(a.queries):
                 flush.fill_(q)
-                b.knnjoin_query(idx, dR, cfg.k, events=ev, **sp[2])
+                out = b.knnjoin_query(idx, dR, cfg.k, want_keys=True, events=ev, **sp[2])
                 torch.cuda.synchronize()
+                if rep == 0 and q == 0:  # every variant's keys must equal the first variant's
+                    if ref_keys is None:
+                        ref_keys = out[2].clone()
+                    elif not torch.equal(out[2], ref_keys):
+                        bad = (out[2] != ref_keys).any(dim=1).sum().item()
+                        print(f"MISMATCH {p}: {bad} rows differ from {a.libs[0]}")
+                        mismatch.add(p)
                 if rep > 0:  # rep 0 warms every variant up
                     times[p].append(ev[0].elapsed_time(ev[1]))
             del idx
@@ -75,7 +83,8 @@ def main():
     base = statistics.median(times[a.libs[0]])
     for p in a.libs:
         m = statistics.median(times[p])
-        print(f"{p:36s} K3 median {m:10.3f} ms  (x{m / base:.3f})  all {[round(t, 3) for t in times[p]]}")
+        tag = "  KEYS DIFFER" if p in mismatch else ""
+        print(f"{p:36s} K3 median {m:10.3f} ms  (x{m / base:.3f})  all {[round(t, 3) for t in times[p]]}{tag}")
 
 
 if __name__ == "__main__":
