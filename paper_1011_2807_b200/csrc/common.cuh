@@ -11,6 +11,15 @@
 
 #define KJ_API extern "C" __attribute__((visibility("default")))
 
+// NVTX range over a C-ABI entry point (SURVEY.md §5 tracing): header-only nvtx3, a no-op unless a tool (nsys, ncu
+// --nvtx) is attached.  The ranges mark host-side enqueue; the kernels they launch carry the same names in traces.
+#include <nvtx3/nvToolsExt.h>
+struct KjNvtxRange {
+  explicit KjNvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~KjNvtxRange() { nvtxRangePop(); }
+};
+#define KJ_NVTX(name) KjNvtxRange kj_nvtx_range_(name)
+
 struct knnjoin_index;
 
 namespace kj {

@@ -219,6 +219,7 @@ KJ_API size_t knnjoin_iiib_profile_bytes(const knnjoin_csr* R, int32_t d) {
 
 KJ_API knnjoin_status knnjoin_iiib_profile(const knnjoin_csr* R, int32_t d, void* profile, size_t profile_bytes,
                                            void* stream) {
+  KJ_NVTX("knnjoin_iiib_profile");
   if (!R || d <= 0 || !profile) { set_error("R / profile NULL or d <= 0"); return KNNJOIN_ERR_ARG; }
   ProfileLayout L;
   if (!profile_layout(d, &L)) { set_error("profile sizing failed"); return KNNJOIN_ERR_ARG; }
@@ -254,6 +255,7 @@ KJ_API size_t knnjoin_iiib_threshold_workspace_bytes(const knnjoin_csr* R) {
 KJ_API knnjoin_status knnjoin_iiib_threshold(const uint64_t* keys, const knnjoin_csr* R, int32_t d,
                                              knnjoin_dtype s_dtype, int32_t k, double* out2, void* workspace,
                                              size_t workspace_bytes, void* stream) {
+  KJ_NVTX("knnjoin_iiib_threshold");
   if (!R || !out2 || d <= 0 || k < 1 || k > kMaxK) { set_error("bad iiib_threshold arguments"); return KNNJOIN_ERR_ARG; }
   if (!workspace || workspace_bytes < knnjoin_iiib_threshold_workspace_bytes(R)) {
     set_error("iiib_threshold workspace too small");
@@ -281,6 +283,7 @@ KJ_API knnjoin_status knnjoin_iiib_split(const knnjoin_csr* S, int32_t d, const 
                                          int32_t r_integer, int64_t* idx_indptr, int32_t* idx_indices,
                                          int8_t* idx_values, int64_t* res_indptr, int32_t* res_indices,
                                          int8_t* res_values, void* workspace, size_t workspace_bytes, void* stream) {
+  KJ_NVTX("knnjoin_iiib_split");
   if (!S || d <= 0 || !profile || !threshold || !idx_indptr || !res_indptr) { set_error("bad iiib_split arguments"); return KNNJOIN_ERR_ARG; }
   if (S->dtype != KNNJOIN_BINARY && S->dtype != KNNJOIN_INT8) { set_error("S must be BINARY or INT8"); return KNNJOIN_ERR_UNSUPPORTED; }
   if (S->nnz > 0 && (!S->indices || !idx_indices || !res_indices ||

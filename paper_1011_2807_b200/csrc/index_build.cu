@@ -583,6 +583,7 @@ KJ_API knnjoin_status knnjoin_build_index(const knnjoin_csr* S, int32_t d, int64
                                           const knnjoin_options* opt, void* storage, size_t storage_bytes,
                                           void* workspace, size_t workspace_bytes, void* stream,
                                           knnjoin_index** out) {
+  KJ_NVTX("knnjoin_build_index");
   if (!out) { set_error("out is NULL"); return KNNJOIN_ERR_ARG; }
   *out = nullptr;
   int32_t tile;

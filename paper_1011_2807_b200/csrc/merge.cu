@@ -172,6 +172,7 @@ KJ_API knnjoin_status knnjoin_merge(const uint64_t* keys, int32_t P, const knnjo
                                     knnjoin_dtype s_dtype, int32_t k, const knnjoin_merge_options* mopt,
                                     uint64_t* out_keys, int32_t* out_ids, float* out_scores,
                                     void* workspace, size_t workspace_bytes, void* stream) {
+  KJ_NVTX("knnjoin_merge");
   if (!R || P < 1 || k < 1 || k > kMaxK) { set_error("bad merge arguments (P %d, k %d)", P, k); return KNNJOIN_ERR_ARG; }
   if (!out_keys && !out_ids && !out_scores) { set_error("no output"); return KNNJOIN_ERR_ARG; }
   if (s_dtype != KNNJOIN_BINARY && s_dtype != KNNJOIN_INT8 && s_dtype != KNNJOIN_FP32) { set_error("bad S dtype"); return KNNJOIN_ERR_ARG; }
@@ -199,6 +200,7 @@ KJ_API knnjoin_status knnjoin_merge(const uint64_t* keys, int32_t P, const knnjo
 static std::mutex g_validate_mu;
 
 KJ_API knnjoin_status knnjoin_validate_csr(const knnjoin_csr* m, int32_t d, void* stream, int64_t* bad_row) {
+  KJ_NVTX("knnjoin_validate_csr");
   if (bad_row) *bad_row = -1;
   if (!m) { set_error("NULL csr"); return KNNJOIN_ERR_ARG; }
   if (d <= 0) { set_error("d must be > 0"); return KNNJOIN_ERR_DIM; }

@@ -538,6 +538,7 @@ KJ_API size_t knnjoin_query_workspace_bytes(const knnjoin_index* idx, const knnj
 KJ_API knnjoin_status knnjoin_query(const knnjoin_index* idx, const knnjoin_csr* R, int32_t k,
                                     const knnjoin_query_options* qopt, uint64_t* out_keys, int32_t* out_ids,
                                     float* out_scores, void* workspace, size_t workspace_bytes, void* stream) {
+  KJ_NVTX("knnjoin_query");
   if (!check_query_args(idx, R, k)) return KNNJOIN_ERR_ARG;
   if (R->n_rows == 0) return KNNJOIN_OK;  // empty R: nothing to write
   if (!out_keys && (!out_ids || !out_scores)) { set_error("need out_keys or both out_ids and out_scores"); return KNNJOIN_ERR_ARG; }

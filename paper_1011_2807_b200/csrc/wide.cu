@@ -466,6 +466,7 @@ using namespace kj;
 KJ_API knnjoin_status knnjoin_certify(const uint64_t* keys, const knnjoin_csr* R, int32_t d, knnjoin_dtype s_dtype,
                                       int32_t k, float tolerance, int32_t* out_list, void* workspace,
                                       size_t workspace_bytes, void* stream) {
+  KJ_NVTX("knnjoin_certify");
   if (!R || k < 1 || k > kMaxK || !out_list) { set_error("bad certify arguments"); return KNNJOIN_ERR_ARG; }
   if (d <= 0) { set_error("d must be > 0"); return KNNJOIN_ERR_DIM; }
   if (s_dtype != KNNJOIN_BINARY && s_dtype != KNNJOIN_INT8) {
