@@ -112,18 +112,15 @@ __device__ __forceinline__ uint64_t block_exclusive_scan_u64(uint64_t v, uint64_
   }
   if (lane == 31) s_warp[warp] = x;
   __syncthreads();
-  if (warp == 0) {
-    uint64_t w = lane < NW ? s_warp[lane] : 0;
+  // every thread adds up the warp totals itself (one barrier instead of a second pass by warp 0 and another barrier)
+  uint64_t before = 0, tot = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w += y;
-    }
-    if (lane < NW) s_warp[lane] = w;  // inclusive warp totals
+  for (int w = 0; w < NW; ++w) {
+    const uint64_t y = s_warp[w];
+    before += w < warp ? y : 0;
+    tot += y;
   }
-  __syncthreads();
-  uint64_t before = warp ? s_warp[warp - 1] : 0;
-  *total = s_warp[NW - 1];
+  *total = tot;
   return before + x - v;
 }
 
