@@ -232,7 +232,11 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
   uint64_t* s_theta = s_warp + NW;           // [B]: max over warps of their k-th key per row
   int* s_misc = (int*)(s_theta + B);         // [0] batch, [1] n sparse items, [2] TOT, [4] U_N (a6/f1)
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // lane from an opaque move: the compiler may not re-materialise it (an S2R + LOP3 per window, whose S2R latency
+  // showed as short-scoreboard stalls in the posting loop)
+  int lane_reg;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(lane_reg));
+  const int tid = threadIdx.x, lane = lane_reg, warp = tid >> 5;
   uint32_t* s_queue = (uint32_t*)(s_misc + 8) + warp * 32;  // this warp's head-completion queue (heads only)
   // a6: bit f set <=> feature f of the batch row is non-essential in the current tile (placed after everything
   // else; the budget only grows within an item, so the bits of earlier tiles stay valid)
