@@ -229,7 +229,11 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
   int32_t* s_qh = s_q;                                                // [kMaxHead][B], aliases staging
   static_assert(kMaxHead * B <= kcap(NW) * B, "q_head must fit in the staging area");
   uint64_t* s_warp = (uint64_t*)(smem + tail_at(B, T, p.k, NW, p.head_smem));
-  uint64_t* s_theta = s_warp + NW;           // [B]: max over warps of their k-th key per row
+  // [B] (u64 slots, low words used): max over the warps of the SCORE of their k-th key per row.  (score << 32) is a
+  // lower bound of that key, so it is a valid admission floor; a 32-bit shared max is one native ATOMS.MAX where the
+  // 64-bit key max was a CAS loop (ATOMS.CAST.SPIN.64)
+  uint64_t* s_theta = s_warp + NW;
+  uint32_t* s_tscore = (uint32_t*)s_theta;
   int* s_misc = (int*)(s_theta + B);         // [0] batch, [1] n sparse items, [2] TOT, [4] U_N (a6/f1)
 
   // lane from an opaque move: the compiler may not re-materialise it (an S2R + LOP3 per window, whose S2R latency
@@ -320,7 +324,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
     }
     if (warp == 0 && lane == 0) {
 #pragma unroll
-      for (int b = 0; b < B; ++b) s_theta[b] = own[b];
+      for (int b = 0; b < B; ++b) s_tscore[b] = (uint32_t)(own[b] >> 32);
     }
     if constexpr (PRUNE)
       for (int i = tid; i < p.prune_words; i += NT_) s_nbits[i] = 0;
@@ -410,7 +414,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
       // value: s_theta is only written during scans, which are fenced by __syncthreads)
       uint32_t budget = 0;
       if constexpr (PRUNE) {
-        const uint32_t th_s = (uint32_t)(*(volatile uint64_t*)&s_theta[0] >> 32);
+        const uint32_t th_s = *(volatile uint32_t*)&s_tscore[0];
         if (th_s > 0) {
           const double a = (double)p.alpha * (double)th_s;
           budget = a >= (double)(th_s - 1) ? th_s - 1 : (uint32_t)a;
@@ -851,7 +855,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
         // theta of row b = max over the warps' k-th keys (k keys at least that large exist in one list, so a
         // candidate key below it cannot be in the row's final top-k; reading c1 total order)
         auto row_theta = [&](int b) {
-          const uint64_t sh = *(volatile uint64_t*)&s_theta[b];
+          const uint64_t sh = (uint64_t)(*(volatile uint32_t*)&s_tscore[b]) << 32;
           return sh > own[b] ? sh : own[b];
         };
         // cheap superset test: key > theta needs score >= t32 (theta's score, +1 when theta's id part admits
@@ -863,7 +867,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
           const uint64_t nk = list_kth<KS>(L[b], k);
           if (nk > own[b]) {
             own[b] = nk;
-            if (lane == 0) atomicMax((unsigned long long*)&s_theta[b], (unsigned long long)nk);
+            if (lane == 0) atomicMax(&s_tscore[b], (uint32_t)(nk >> 32));
           }
         };
         uint64_t th[B];
