@@ -505,7 +505,9 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
               const int e = e_cur + __popc(M & (lt_mask | (1u << lane)));
               const int e_next = e_cur + __popc(M) + (__ballot_sync(0xffffffffu, o == 32) ? 1 : 0);
               e_cur = min(e_next, n_items - 1);
-              KJ_CHECK(e >= 0 && e < n_items);
+              // lanes past the warp's last unit (tail of the last window) may count the end of the stream as a
+              // start (e == n_items); their entry is clamped and stage C skips them
+              KJ_CHECK(e >= 0 && (e < n_items || m * 32 + (uint32_t)lane >= tot));
               const uint2 bq = w_bq[min(e, n_items - 1)];
               pS = ldP();
               return bq;
