@@ -519,8 +519,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
                 const uint32_t unit = bq.x + pp;
                 KJ_CHECK((int64_t)unit < p.unit_cap);
                 S.q = bq.y;
-                S.id = ldg_nc_v4(p.ids + (size_t)unit * 8, l2pol);
                 if (wint8) S.w = ldg_nc_v2(p.vals + (size_t)unit * 8, l2pol);
+                S.id = ldg_nc_v4(p.ids + (size_t)unit * 8, l2pol);
               }
             };
             auto process = [&](const St& S) {
@@ -549,16 +549,18 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
               D[j].q = 0;
               D[j].v = false;
             }
+            // each slot is refilled right after it is processed, so the loads of LD + 1 windows are in flight
+            // while one is processed and a window's loads are issued LD + 1 steps before their use
             uint32_t pS = ldP();
 #pragma unroll
-            for (int j = 0; j < LD; ++j) stC(j, stR(j, pS), D[j]);
-            uint2 bqC = stR(LD, pS);
+            for (int j = 0; j <= LD; ++j) stC(j, stR(j, pS), D[j]);
+            uint2 bqC = stR(LD + 1, pS);
             for (uint32_t w = 0; w < wend; w += LD + 1) {
 #pragma unroll
               for (int j = 0; j <= LD; ++j) {
-                stC(w + j + LD, bqC, D[(j + LD) % (LD + 1)]);
-                bqC = stR(w + j + LD + 1, pS);
                 process(D[j]);
+                stC(w + j + LD + 1, bqC, D[j]);
+                bqC = stR(w + j + LD + 2, pS);
               }
             }
           }
