@@ -1034,7 +1034,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
                 }
               }
             }
-            const int npend = __reduce_add_sync(0xffffffffu, __popc(pend));
+            // usually no pair of the step can reach theta: one vote, and the count (REDUX) only when some can
+            const int npend = __any_sync(0xffffffffu, pend != 0u) ? __reduce_add_sync(0xffffffffu, __popc(pend)) : 0;
             if (npend > 32) {
               // many pairs may reach theta (the first tiles of a batch, theta still low): complete every pair
               // from the tables and take the plain filter below
