@@ -1014,10 +1014,20 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUN
             const uint32_t hw[4] = {hq.x, hq.y, hq.z, hq.w};
             if (c + 128 < cols) hq = __ldg((const uint4*)(hcols + c + 128));  // next step's head words
             uint32_t pend = 0;  // bit 4b+j: pair (row b, column col+j) may reach theta
+            uint32_t tsb[B];    // the rows' shared floors, one 64-bit load for two rows
+            if constexpr (B == 2) {
+              const unsigned long long t2 = *(volatile unsigned long long*)s_tscore;
+              tsb[0] = (uint32_t)t2;
+              tsb[1] = (uint32_t)(t2 >> 32);
+            } else {
+#pragma unroll
+              for (int b = 0; b < B; ++b) tsb[b] = *(volatile uint32_t*)&s_tscore[b];
+            }
 #pragma unroll
             for (int b = 0; b < B; ++b) {
               if (b < nb) {
-                th[b] = row_theta(b);
+                const uint64_t sh = (uint64_t)tsb[b] << 32;
+                th[b] = sh > own[b] ? sh : own[b];
                 const uint32_t t32 = t32_of(th[b]);
                 const uint32_t hm = hmr[b];
                 const uint32_t* cum = s_cum + b * (kMaxHead + 1);
