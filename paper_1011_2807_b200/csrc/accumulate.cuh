@@ -203,7 +203,7 @@ __device__ __forceinline__ void red_add_shared(uint32_t addr, uint32_t v) {
 // U_N = sum of c over N's non-empty slices of the tile; any other s has score <= x + U_N < theta (or, with
 // x = 0, <= U_N <= budget < theta) and cannot enter.
 template <int B, int KS, bool SINT8, int NW, bool HEADS, bool PRUNE = false>
-__global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUNE) ? (KS >= 4 ? 4 : 5) : 6) : (NW == 8 ? 3 : 1))
+__global__ void __launch_bounds__(NW * 32, NW == 4 ? ((B == 1 && !HEADS && !PRUNE) ? (KS >= 4 ? 4 : 5) : 6) : (NW == 8 ? (KS >= 8 ? 2 : 3) : 1))
     k_accumulate_topk(QP p) {
   static_assert(!PRUNE || (B == 1 && !HEADS), "pruned instances are one-row and head-free");
   constexpr bool ROWP = B == 1 && !HEADS && !PRUNE;  // one-row head-free instance: per-warp accumulate

@@ -35,11 +35,13 @@ def main():
     ap.add_argument("--rows-s", type=int, default=0)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--queries", type=int, default=2)
+    ap.add_argument("--k", type=int, default=0, help="override the config's k")
     a = ap.parse_args()
     cfg = gen.CONFIGS[a.config]
     if a.rows_r or a.rows_s:
         cfg = cfg.scaled(a.rows_r or None, a.rows_s or None)
     R, S = gen.generate(cfg, "R"), gen.generate(cfg, "S")
+    k = a.k or cfg.k
     dR, dS = b.DeviceCSR.from_host(R), b.DeviceCSR.from_host(S)
     # variant spec: path[:key=val,key=val...] with build keys (tile, head_max, head_density) and query keys
     # (batch_rows, cta_warps, tiles_per_pass, row_order)
@@ -67,7 +69,7 @@ def main():
                 e.record()
             for q in range(a.queries):
                 flush.fill_(q)
-                out = b.knnjoin_query(idx, dR, cfg.k, want_keys=True, events=ev, **sp[2])
+                out = b.knnjoin_query(idx, dR, k, want_keys=True, events=ev, **sp[2])
                 torch.cuda.synchronize()
                 if rep == 0 and q == 0:  # every variant's keys must equal the first variant's
                     if ref_keys is None:
